@@ -1,0 +1,647 @@
+// api.cu — the C-ABI of include/fastpfp.h: handle state, device memory layout and the host-side
+// orchestration of Algorithm 1. All arithmetic of the path runs in the kernels of
+// proj.cu / gemm_simt.cu / gemm_tc.cu / discretize.cu; this file only allocates, validates,
+// launches and copies.
+//
+// Device layout: every matrix is fp32 row-major with its row stride rounded
+// up to 32 floats (128 B) so rows are 16 B aligned for float4 / TMA access; padding is zero.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fastpfp.h"
+#include "common.cuh"
+
+using namespace fpfp;
+
+namespace {
+
+constexpr int kMaxCheck = 64;  // max outer iterations per host convergence check
+
+struct Buf {
+  float* p = nullptr;
+  int64_t ld = 0;
+  int rows = 0, cols = 0;
+};
+
+}  // namespace
+
+struct fastpfp_handle {
+  int64_t n = 0, np = 0, d = 0, m = 0;
+  int device = 0, num_sms = 0, arch = 0;
+  // graphs and their TF32 splits
+  Buf A, Ab, As, Ap, Apb, Aps, B, Bp, K;
+  // state
+  Buf X, Xb, Xs, X0, U, Ub, Us, Y, G;  // G: objective scratch (lazy)
+  // projection scratch
+  double *rowpart = nullptr, *colpart = nullptr, *r = nullptr, *c = nullptr;
+  double *sig_part = nullptr, *mu_part = nullptr;
+  float *dlt_part = nullptr, *rho_part = nullptr;
+  int TR = 8, RB = 1, CB = 1, RBx = 1, CBx = 1, grid = 1;
+  DevIter* iters = nullptr;       // [kMaxCheck] device
+  DevIter* h_iters = nullptr;     // pinned mirror
+  int* done = nullptr;            // device flag
+  int* flags = nullptr;           // validation flags (device)
+  double* scal = nullptr;         // device scalars (objective)
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int slack_mode = 0, precision = 2, rescale = 1, check_every = 4;
+  bool graphs_set = false, x0_custom = false, poisoned = false;
+  int64_t t = 0;
+  std::string err;
+  // stats / profiling
+  fastpfp_stats stats{};
+  int profile = 0;
+  cudaEvent_t ev[3 * kMaxCheck] = {};
+  bool ev_ready = false;
+};
+
+namespace {
+
+int set_err(fastpfp_handle* h, int code, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+    if (code == FASTPFP_ECUDA || code == FASTPFP_ENCCL) h->poisoned = true;
+  }
+  return code;
+}
+
+#define CK(h, call)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err((h), e_ == cudaErrorMemoryAllocation ? FASTPFP_ENOMEM : FASTPFP_ECUDA, \
+                     "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,       \
+                     __LINE__);                                                              \
+  } while (0)
+
+#define GUARD(h)                                                             \
+  do {                                                                       \
+    if (!(h)) return FASTPFP_EINVAL;                                         \
+    if ((h)->poisoned) return FASTPFP_EPOISONED;                             \
+    cudaError_t e0_ = cudaSetDevice((h)->device);                            \
+    if (e0_ != cudaSuccess) return set_err((h), FASTPFP_ECUDA, "cudaSetDevice: %s", \
+                                           cudaGetErrorString(e0_));        \
+  } while (0)
+
+cudaError_t alloc_buf(Buf& b, int rows, int cols) {
+  b.rows = rows;
+  b.cols = cols;
+  b.ld = round_up(std::max(cols, 1), 32);
+  size_t bytes = (size_t)std::max(rows, 1) * b.ld * sizeof(float);
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) return e;
+  return cudaMemset(b.p, 0, bytes);
+}
+
+void free_buf(Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+}
+
+template <typename T>
+cudaError_t alloc_arr(T*& p, size_t count) {
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// dense (ld = cols) host/device matrix -> padded device buffer
+cudaError_t upload(const Buf& b, const float* src, int is_device, cudaStream_t s) {
+  return cudaMemcpy2DAsync(b.p, b.ld * sizeof(float), src, (size_t)b.cols * sizeof(float),
+                           (size_t)b.cols * sizeof(float), b.rows,
+                           is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+}
+
+cudaError_t download(const Buf& b, float* dst, int is_device, cudaStream_t s) {
+  return cudaMemcpy2DAsync(dst, (size_t)b.cols * sizeof(float), b.p, b.ld * sizeof(float),
+                           (size_t)b.cols * sizeof(float), b.rows,
+                           is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
+}
+
+// projection tiling: largest TR in {128, 64, 32, 16, 8} giving >= 2 tiles per SM, else 8
+void plan_projection(fastpfp_handle* h) {
+  const int64_t m = h->m;
+  const int CB = (int)ceil_div(m, kProjTC);
+  int TR = 8;
+  for (int tr : {128, 64, 32, 16, 8}) {
+    if (ceil_div(m, tr) * CB >= 2LL * h->num_sms) { TR = tr; break; }
+  }
+  h->TR = TR;
+  h->CB = CB;
+  h->RB = (int)ceil_div(m, TR);
+  h->RBx = (int)ceil_div(h->n, TR);
+  h->CBx = (int)ceil_div(h->np, kProjTC);
+  const int64_t want = std::max<int64_t>((int64_t)h->RB * h->CB, (int64_t)h->RBx * h->CBx);
+  const int maxg = proj_max_grid(h->device);
+  h->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, maxg));
+}
+
+int run_gemm(fastpfp_handle* h, GemmArgs& g) {
+  cudaError_t e;
+  h->stats.launches += 1;
+  h->stats.gemm_launches += 1;
+  if (h->precision == 2 || !gemm_tc_supported(g)) {
+    if (h->precision != 2)
+      return set_err(h, FASTPFP_EUNSUPPORTED, "tensor-core GEMM does not support M=%d N=%d K=%d",
+                     g.M, g.N, g.K);
+    e = launch_gemm_simt(g, h->stream);
+  } else {
+    e = launch_gemm_tc(g, h->precision == 1 ? 1 : 3, h->stream, h->device);
+  }
+  CK(h, e);
+  return FASTPFP_OK;
+}
+
+// X <- X0, split, Y <- 0, t <- 0
+int reset_state(fastpfp_handle* h) {
+  cudaStream_t s = h->stream;
+  if (h->x0_custom) {
+    CK(h, cudaMemcpy2DAsync(h->X.p, h->X.ld * 4, h->X0.p, h->X0.ld * 4, h->np * 4, h->n,
+                            cudaMemcpyDeviceToDevice, s));
+  } else {
+    CK(h, launch_fill(h->X.p, h->X.ld, (int)h->n, (int)h->np,
+                      (float)(1.0 / ((double)h->n * (double)h->np)), s));  // 11^T/(nn')
+  }
+  CK(h, launch_split(h->X.p, h->X.ld, h->Xb.p, h->Xs.p, h->X.ld, (int)h->n, (int)h->np, s));
+  CK(h, cudaMemsetAsync(h->Y.p, 0, (size_t)h->m * h->Y.ld * sizeof(float), s));  // Y = 0
+  CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
+  CK(h, cudaStreamSynchronize(s));
+  h->t = 0;
+  return FASTPFP_OK;
+}
+
+int check_flags(fastpfp_handle* h, const char* what) {
+  int f = 0;
+  CK(h, cudaMemcpyAsync(&f, h->flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (f & 2) return set_err(h, FASTPFP_ENONFINITE, "%s contains NaN/Inf", what);
+  if (f & 1) return set_err(h, FASTPFP_ESYM, "%s is not symmetric (undirected graphs, P:135-136)", what);
+  return FASTPFP_OK;
+}
+
+}  // namespace
+
+int fpfp_discretize_device(fastpfp_handle*, const float*, int64_t, int, int, int32_t*,
+                           cudaStream_t, std::string&);
+
+extern "C" {
+
+const char* fastpfp_status_string(int s) {
+  switch (s) {
+    case FASTPFP_OK: return "ok";
+    case FASTPFP_EINVAL: return "invalid argument";
+    case FASTPFP_ESYM: return "adjacency matrix not symmetric";
+    case FASTPFP_ENONFINITE: return "non-finite input";
+    case FASTPFP_ESTATE: return "call order (set_graphs first)";
+    case FASTPFP_ENOMEM: return "device out of memory";
+    case FASTPFP_ECUDA: return "CUDA error";
+    case FASTPFP_ENCCL: return "NCCL error";
+    case FASTPFP_ENODEV: return "no sm_100 device";
+    case FASTPFP_EPOISONED: return "handle poisoned by an earlier CUDA/NCCL error";
+    case FASTPFP_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+int fastpfp_abi_version(void) { return FASTPFP_ABI_VERSION; }
+
+int fastpfp_device_arch(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major * 10 + minor;
+}
+
+const char* fastpfp_last_error(const fastpfp_handle* h) { return h ? h->err.c_str() : ""; }
+
+void fastpfp_destroy(fastpfp_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (Buf* b : {&h->A, &h->Ab, &h->As, &h->Ap, &h->Apb, &h->Aps, &h->B, &h->Bp, &h->K, &h->X,
+                 &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G})
+    free_buf(*b);
+  for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
+                  (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
+                  (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal})
+    if (p) cudaFree(p);
+  if (h->h_iters) cudaFreeHost(h->h_iters);
+  if (h->ev_ready)
+    for (auto& e : h->ev) cudaEventDestroy(e);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) {
+  if (!out || n < 1 || n_prime < 1 || d < 0 || n > (1 << 20) || n_prime > (1 << 20) ||
+      d > (1 << 20))
+    return FASTPFP_EINVAL;
+  *out = nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FASTPFP_ENODEV;
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return FASTPFP_ENODEV;
+  fastpfp_handle* h = new fastpfp_handle();
+  h->n = n; h->np = n_prime; h->d = d; h->m = std::max(n, n_prime);
+  h->device = dev;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  h->arch = fastpfp_device_arch();
+  int rc = FASTPFP_OK;
+  auto A = [&](cudaError_t e) {
+    if (e != cudaSuccess && rc == FASTPFP_OK)
+      rc = (e == cudaErrorMemoryAllocation) ? FASTPFP_ENOMEM : FASTPFP_ECUDA;
+  };
+  const int N = (int)n, NP = (int)n_prime, M = (int)h->m, D = (int)d;
+  A(alloc_buf(h->A, N, N)); A(alloc_buf(h->Ab, N, N)); A(alloc_buf(h->As, N, N));
+  A(alloc_buf(h->Ap, NP, NP)); A(alloc_buf(h->Apb, NP, NP)); A(alloc_buf(h->Aps, NP, NP));
+  if (D > 0) { A(alloc_buf(h->B, N, D)); A(alloc_buf(h->Bp, NP, D)); }
+  A(alloc_buf(h->K, N, NP));
+  A(alloc_buf(h->X, N, NP)); A(alloc_buf(h->Xb, N, NP)); A(alloc_buf(h->Xs, N, NP));
+  A(alloc_buf(h->U, NP, N)); A(alloc_buf(h->Ub, NP, N)); A(alloc_buf(h->Us, NP, N));
+  A(alloc_buf(h->Y, M, M));
+  plan_projection(h);
+  A(alloc_arr(h->rowpart, (size_t)h->CB * M));
+  A(alloc_arr(h->colpart, (size_t)h->RB * M));
+  A(alloc_arr(h->r, M)); A(alloc_arr(h->c, M));
+  A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
+  A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
+  A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
+  A(alloc_arr(h->scal, 4));
+  A(cudaMallocHost(&h->h_iters, kMaxCheck * sizeof(DevIter)));
+  A(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  if (rc != FASTPFP_OK) {
+    cudaGetLastError();
+    fastpfp_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return FASTPFP_OK;
+}
+
+int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
+  GUARD(h);
+  switch (key) {
+    case FASTPFP_OPT_SLACK_MODE:
+      if (value != 0 && value != 1) return FASTPFP_EINVAL;
+      h->slack_mode = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_PRECISION:
+      if (value < 0 || value > 2) return FASTPFP_EINVAL;
+      h->precision = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_RESCALE:
+      if (value != 0 && value != 1) return FASTPFP_EINVAL;
+      h->rescale = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_STREAM:
+      CK(h, cudaStreamSynchronize(h->stream));
+      if (h->own_stream) cudaStreamDestroy(h->stream);
+      h->own_stream = value == 0;
+      if (value == 0) {
+        CK(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      } else {
+        h->stream = reinterpret_cast<cudaStream_t>(value);
+      }
+      return FASTPFP_OK;
+    case FASTPFP_OPT_CHECK_EVERY:
+      if (value < 1 || value > kMaxCheck) return FASTPFP_EINVAL;
+      h->check_every = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_PROFILE:
+      if (value != 0 && value != 1) return FASTPFP_EINVAL;
+      if (value && !h->ev_ready) {
+        for (auto& e : h->ev) CK(h, cudaEventCreate(&e));
+        h->ev_ready = true;
+      }
+      h->profile = (int)value; return FASTPFP_OK;
+  }
+  return set_err(h, FASTPFP_EINVAL, "unknown option key %d", key);
+}
+
+int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, const float* B,
+                       const float* B_prime, int is_device) {
+  GUARD(h);
+  if (!A || !A_prime) return set_err(h, FASTPFP_EINVAL, "A and A' are required");
+  if (h->d > 0 && (!B || !B_prime)) return set_err(h, FASTPFP_EINVAL, "B and B' required (d > 0)");
+  cudaStream_t s = h->stream;
+  h->graphs_set = false;
+  CK(h, upload(h->A, A, is_device, s));
+  CK(h, upload(h->Ap, A_prime, is_device, s));
+  CK(h, cudaMemsetAsync(h->flags, 0, sizeof(int), s));
+  CK(h, launch_check_sym(h->A.p, h->A.ld, (int)h->n, h->flags, s));
+  int rc = check_flags(h, "A");
+  if (rc) return rc;
+  CK(h, launch_check_sym(h->Ap.p, h->Ap.ld, (int)h->np, h->flags, s));
+  rc = check_flags(h, "A'");
+  if (rc) return rc;
+  CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n, s));
+  CK(h, launch_split(h->Ap.p, h->Ap.ld, h->Apb.p, h->Aps.p, h->Ap.ld, (int)h->np, (int)h->np, s));
+  if (h->d > 0) {
+    CK(h, upload(h->B, B, is_device, s));
+    CK(h, upload(h->Bp, B_prime, is_device, s));
+    CK(h, launch_check_finite(h->B.p, h->B.ld, (int)h->n, (int)h->d, h->flags, s));
+    CK(h, launch_check_finite(h->Bp.p, h->Bp.ld, (int)h->np, (int)h->d, h->flags, s));
+    rc = check_flags(h, "B/B'");
+    if (rc) return rc;
+    // K = B B'^T in fp32 (SIMT; d is small)
+    GemmArgs g{};
+    g.P = h->B.p; g.ldP = h->B.ld; g.Q = h->Bp.p; g.ldQ = h->Bp.ld;
+    g.M = (int)h->n; g.N = (int)h->np; g.K = (int)h->d;
+    g.epi = kEpiPlain; g.C = h->K.p; g.ldC = h->K.ld;
+    CK(h, launch_gemm_simt(g, s));
+  } else {
+    CK(h, cudaMemsetAsync(h->K.p, 0, (size_t)h->n * h->K.ld * sizeof(float), s));
+  }
+  rc = reset_state(h);
+  if (rc) return rc;
+  h->graphs_set = true;
+  return FASTPFP_OK;
+}
+
+int fastpfp_set_x0(fastpfp_handle* h, const float* X0, int is_device) {
+  GUARD(h);
+  cudaStream_t s = h->stream;
+  if (X0) {
+    if (!h->X0.p) CK(h, alloc_buf(h->X0, (int)h->n, (int)h->np));
+    CK(h, upload(h->X0, X0, is_device, s));
+    CK(h, cudaMemsetAsync(h->flags, 0, sizeof(int), s));
+    CK(h, launch_check_finite(h->X0.p, h->X0.ld, (int)h->n, (int)h->np, h->flags, s));
+    int rc = check_flags(h, "X0");
+    if (rc) return rc;
+    h->x0_custom = true;
+  } else {
+    h->x0_custom = false;
+  }
+  return reset_state(h);
+}
+
+int fastpfp_reset(fastpfp_handle* h) {
+  GUARD(h);
+  return reset_state(h);
+}
+
+int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1, double eps2,
+                    int32_t max_iter1, int32_t max_iter2, float* X_out, fastpfp_report* rep) {
+  GUARD(h);
+  if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
+  if (!(alpha >= 0.0 && alpha <= 1.0) || !(lambda >= 0.0) || !std::isfinite(lambda) ||
+      !(eps1 >= 0.0) || !(eps2 >= 0.0) || max_iter1 < 1 || max_iter2 < 1)
+    return set_err(h, FASTPFP_EINVAL, "alpha in [0,1], lambda >= 0, eps >= 0, maxIter >= 1");
+  cudaStream_t s = h->stream;
+  fastpfp_report R{};
+  if (rep) {
+    R.trace_capacity = rep->trace_capacity;
+    R.rho_trace = rep->rho_trace; R.sweeps_trace = rep->sweeps_trace;
+    R.delta_trace = rep->delta_trace; R.mu_trace = rep->mu_trace;
+  }
+  CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
+  const int N = (int)h->n, NP = (int)h->np;
+  int32_t left = max_iter1;
+  bool stop = false;
+  while (left > 0 && !stop) {
+    const int chunk = std::min<int32_t>(left, h->check_every);
+    CK(h, cudaMemsetAsync(h->iters, 0, chunk * sizeof(DevIter), s));
+    for (int k = 0; k < chunk; ++k) {
+      if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k], s));
+      // Algorithm 1 line 3: U = A' X^T (= (X A')^T, A' symmetric) ...
+      GemmArgs g1{};
+      g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
+      g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
+      g1.M = NP; g1.N = N; g1.K = NP;
+      g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.C3 = h->U.p; g1.ldC = h->U.ld;
+      g1.done = h->done;
+      int rc = run_gemm(h, g1);
+      if (rc) return rc;
+      // ... then Y[0:n, 0:n'] = A U^T + lambda K = A X A' + lambda K
+      GemmArgs g2{};
+      g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
+      g2.Q = h->U.p; g2.ldQ = h->U.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
+      g2.M = N; g2.N = NP; g2.K = N;
+      g2.epi = kEpiAxpy; g2.C = h->Y.p; g2.ldC = h->Y.ld;
+      g2.D = (lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
+      g2.lam = (float)lambda;
+      g2.done = h->done;
+      rc = run_gemm(h, g2);
+      if (rc) return rc;
+      if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 1], s));
+      if (h->slack_mode == 1 && h->m > std::min(h->n, h->np)) {
+        CK(h, launch_zero_slack(h->Y.p, h->Y.ld, (int)h->m, N, NP, h->done, s));
+        h->stats.launches += 1;
+      }
+      // lines 4-9: projection loop, blend, rescale (one persistent kernel)
+      ProjArgs pa{};
+      pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
+      pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = N; pa.np = NP;
+      pa.alpha = alpha; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = max_iter2;
+      pa.rescale = h->rescale; pa.split = 1; pa.do_finalize = 1; pa.do_sums = 1;
+      pa.TR = h->TR; pa.RB = h->RB; pa.CB = h->CB; pa.RBx = h->RBx; pa.CBx = h->CBx;
+      pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c;
+      pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;
+      pa.rho_part = h->rho_part; pa.iter_out = h->iters + k; pa.done = h->done;
+      CK(h, launch_proj(pa, h->grid, s));
+      h->stats.launches += 1;
+      h->stats.proj_launches += 1;
+      if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 2], s));
+    }
+    CK(h, cudaMemcpyAsync(h->h_iters, h->iters, chunk * sizeof(DevIter), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    for (int k = 0; k < chunk; ++k) {
+      const DevIter& it = h->h_iters[k];
+      if (!it.valid) { stop = true; break; }
+      if (h->profile) {
+        float g_ms = 0.f, p_ms = 0.f;
+        CK(h, cudaEventElapsedTime(&g_ms, h->ev[3 * k], h->ev[3 * k + 1]));
+        CK(h, cudaEventElapsedTime(&p_ms, h->ev[3 * k + 1], h->ev[3 * k + 2]));
+        h->stats.gemm_ms += g_ms;
+        h->stats.proj_ms += p_ms;
+        h->stats.gemm_flops += 2.0 * (double)N * NP * ((double)N + NP);
+      }
+      h->stats.outer_iterations += 1;
+      h->stats.sweeps += it.sweeps;
+      R.total_sweeps += it.sweeps;
+      R.last_delta = it.delta;
+      R.last_mu = it.mu;
+      if (it.degenerate) { R.degenerate = 1; stop = true; break; }
+      if (R.trace_capacity > R.iterations) {
+        const int q = R.iterations;
+        if (R.rho_trace) R.rho_trace[q] = it.rho;
+        if (R.sweeps_trace) R.sweeps_trace[q] = it.sweeps;
+        if (R.delta_trace) R.delta_trace[q] = it.delta;
+        if (R.mu_trace) R.mu_trace[q] = it.mu;
+      }
+      R.iterations += 1;
+      R.last_rho = it.rho;
+      h->t += 1;
+      if (it.converged) { R.converged = 1; stop = true; break; }
+    }
+    left -= chunk;
+  }
+  if (X_out) {
+    CK(h, download(h->X, X_out, 0, s));
+    CK(h, cudaStreamSynchronize(s));
+  }
+  if (rep) *rep = R;
+  return FASTPFP_OK;
+}
+
+int fastpfp_get_stats(fastpfp_handle* h, fastpfp_stats* out) {
+  GUARD(h);
+  if (!out) return FASTPFP_EINVAL;
+  *out = h->stats;
+  return FASTPFP_OK;
+}
+
+int fastpfp_reset_stats(fastpfp_handle* h) {
+  GUARD(h);
+  h->stats = fastpfp_stats{};
+  return FASTPFP_OK;
+}
+
+int fastpfp_copy_x(fastpfp_handle* h, float* dst, int dst_is_device) {
+  GUARD(h);
+  if (!dst) return FASTPFP_EINVAL;
+  CK(h, download(h->X, dst, dst_is_device, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return FASTPFP_OK;
+}
+
+int fastpfp_copy_y(fastpfp_handle* h, float* dst, int dst_is_device) {
+  GUARD(h);
+  if (!dst) return FASTPFP_EINVAL;
+  CK(h, download(h->Y, dst, dst_is_device, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return FASTPFP_OK;
+}
+
+int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
+  GUARD(h);
+  if (!f) return FASTPFP_EINVAL;
+  if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
+  if (!h->G.p) CK(h, alloc_buf(h->G, (int)h->n, (int)h->np));
+  cudaStream_t s = h->stream;
+  const int N = (int)h->n, NP = (int)h->np;
+  GemmArgs g1{};
+  g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
+  g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
+  g1.M = NP; g1.N = N; g1.K = NP;
+  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.C3 = h->U.p; g1.ldC = h->U.ld;
+  int rc = run_gemm(h, g1);
+  if (rc) return rc;
+  GemmArgs g2{};
+  g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
+  g2.Q = h->U.p; g2.ldQ = h->U.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
+  g2.M = N; g2.N = NP; g2.K = N;
+  g2.epi = kEpiAxpy; g2.C = h->G.p; g2.ldC = h->G.ld; g2.D = nullptr;
+  rc = run_gemm(h, g2);
+  if (rc) return rc;
+  CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, N, NP, h->scal, s));
+  double v[2];
+  CK(h, cudaMemcpyAsync(v, h->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  *f = 0.5 * v[0] + lambda * v[1];  // 1/2 tr(X^T A X A') + lambda tr(X^T K)
+  return FASTPFP_OK;
+}
+
+int fastpfp_discretize(fastpfp_handle* h, int32_t* assign) {
+  GUARD(h);
+  if (!assign) return FASTPFP_EINVAL;
+  if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
+  std::string msg;
+  int rc = fpfp_discretize_device(h, h->X.p, h->X.ld, (int)h->n, (int)h->np, assign, h->stream, msg);
+  if (rc) return set_err(h, rc, "%s", msg.c_str());
+  return FASTPFP_OK;
+}
+
+int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t* sweeps_out,
+                    double* delta_out, int64_t stream) {
+  if (!Y || m < 1 || max_iter2 < 1 || !(eps2 >= 0.0)) return FASTPFP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FASTPFP_ENODEV;
+  fastpfp_handle tmp;
+  tmp.n = m; tmp.np = m; tmp.m = m; tmp.device = dev;
+  cudaDeviceGetAttribute(&tmp.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  plan_projection(&tmp);
+  Buf Yp;
+  int rc = FASTPFP_OK;
+  DevIter it{};
+  auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
+  A(alloc_buf(Yp, (int)m, (int)m));
+  A(alloc_arr(tmp.rowpart, (size_t)tmp.CB * m)); A(alloc_arr(tmp.colpart, (size_t)tmp.RB * m));
+  A(alloc_arr(tmp.r, m)); A(alloc_arr(tmp.c, m));
+  A(alloc_arr(tmp.sig_part, tmp.grid)); A(alloc_arr(tmp.mu_part, tmp.grid));
+  A(alloc_arr(tmp.dlt_part, tmp.grid)); A(alloc_arr(tmp.rho_part, tmp.grid));
+  A(alloc_arr(tmp.iters, 1)); A(alloc_arr(tmp.done, 1));
+  if (rc == FASTPFP_OK) {
+    A(upload(Yp, Y, 1, s));
+    ProjArgs pa{};
+    pa.Y = Yp.p; pa.ldY = Yp.ld; pa.m = (int)m; pa.n = (int)m; pa.np = (int)m;
+    pa.eps2 = eps2; pa.max_iter2 = max_iter2; pa.do_finalize = 0; pa.do_sums = 1;
+    pa.TR = tmp.TR; pa.RB = tmp.RB; pa.CB = tmp.CB; pa.RBx = tmp.RBx; pa.CBx = tmp.CBx;
+    pa.rowpart = tmp.rowpart; pa.colpart = tmp.colpart; pa.r = tmp.r; pa.c = tmp.c;
+    pa.sig_part = tmp.sig_part; pa.dlt_part = tmp.dlt_part; pa.mu_part = tmp.mu_part;
+    pa.rho_part = tmp.rho_part; pa.iter_out = tmp.iters; pa.done = tmp.done;
+    A(launch_proj(pa, tmp.grid, s));
+    A(download(Yp, Y, 1, s));
+    A(cudaMemcpyAsync(&it, tmp.iters, sizeof(DevIter), cudaMemcpyDeviceToHost, s));
+    A(cudaStreamSynchronize(s));
+  }
+  free_buf(Yp);
+  for (void* p : {(void*)tmp.rowpart, (void*)tmp.colpart, (void*)tmp.r, (void*)tmp.c,
+                  (void*)tmp.sig_part, (void*)tmp.mu_part, (void*)tmp.dlt_part,
+                  (void*)tmp.rho_part, (void*)tmp.iters, (void*)tmp.done})
+    if (p) cudaFree(p);
+  tmp.rowpart = tmp.colpart = tmp.r = tmp.c = tmp.sig_part = tmp.mu_part = nullptr;
+  tmp.dlt_part = tmp.rho_part = nullptr; tmp.iters = nullptr; tmp.done = nullptr;
+  if (rc == FASTPFP_OK) {
+    if (sweeps_out) *sweeps_out = it.sweeps;
+    if (delta_out) *delta_out = it.delta;
+  }
+  return rc;
+}
+
+int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
+                    int precision, int64_t stream) {
+  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || precision < 0 || precision > 2)
+    return FASTPFP_EINVAL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FASTPFP_ENODEV;
+  Buf Pp, Pb, Ps, Qp, Qb, Qs, Cp;
+  int rc = FASTPFP_OK;
+  auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
+  A(alloc_buf(Pp, (int)M, (int)K)); A(alloc_buf(Pb, (int)M, (int)K)); A(alloc_buf(Ps, (int)M, (int)K));
+  A(alloc_buf(Qp, (int)N, (int)K)); A(alloc_buf(Qb, (int)N, (int)K)); A(alloc_buf(Qs, (int)N, (int)K));
+  A(alloc_buf(Cp, (int)M, (int)N));
+  if (rc == FASTPFP_OK) {
+    A(upload(Pp, P, 1, s)); A(upload(Qp, Q, 1, s));
+    A(launch_split(Pp.p, Pp.ld, Pb.p, Ps.p, Pp.ld, (int)M, (int)K, s));
+    A(launch_split(Qp.p, Qp.ld, Qb.p, Qs.p, Qp.ld, (int)N, (int)K, s));
+    GemmArgs g{};
+    g.P = Pp.p; g.ldP = Pp.ld; g.Pb = Pb.p; g.Ps = Ps.p;
+    g.Q = Qp.p; g.ldQ = Qp.ld; g.Qb = Qb.p; g.Qs = Qs.p;
+    g.M = (int)M; g.N = (int)N; g.K = (int)K; g.epi = kEpiPlain; g.C = Cp.p; g.ldC = Cp.ld;
+    if (precision == 2) {
+      A(launch_gemm_simt(g, s));
+    } else if (!gemm_tc_supported(g)) {
+      rc = FASTPFP_EUNSUPPORTED;
+    } else {
+      A(launch_gemm_tc(g, precision == 1 ? 1 : 3, s, dev));
+    }
+    if (rc == FASTPFP_OK) A(download(Cp, C, 1, s));
+    A(cudaStreamSynchronize(s));
+  }
+  for (Buf* b : {&Pp, &Pb, &Ps, &Qp, &Qb, &Qs, &Cp}) free_buf(*b);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// common.cuh — shared device helpers and internal declarations of the FastPFP B200 library.
+// Everything here is product code (no oracle); see include/fastpfp.h for the public contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fpfp {
+
+constexpr int kWarp = 32;
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
+__host__ __device__ inline int64_t ceil_div(int64_t x, int64_t q) { return (x + q - 1) / q; }
+
+// TF32 round-to-nearest (ties away), the split used by the 3xTF32 GEMM: a = big + small with
+// big = rna_tf32(a), small = rna_tf32(a - big) (a - big is exact in fp32).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Per-outer-iteration record written by the projection/finalize kernel (device memory).
+struct DevIter {
+  int32_t valid;       // 1 if this outer iteration ran (X updated or degenerate detected)
+  int32_t sweeps;      // projection sweeps made
+  int32_t degenerate;  // max(X~) <= 1e-300
+  int32_t converged;   // rho < eps1
+  double delta;        // last sweep's max|dY|
+  double mu;           // max(X~)
+  double rho;          // max|X_new - X_old|
+};
+
+// Arguments of the persistent projection + finalize kernel (proj.cu).
+struct ProjArgs {
+  float* Y; int64_t ldY; int m;                // slacked matrix, m x m (row stride ldY, 16B rows)
+  float* X; float* Xb; float* Xs; int64_t ldX; // soft assignment n x n' and its TF32 split
+  int n, np;
+  double alpha, eps1, eps2;
+  int max_iter2;
+  int rescale, split, do_finalize, do_sums;
+  int TR, RB, CB;        // sweep tiles: TR rows x 512 cols over m x m
+  int RBx, CBx;          // finalize tiles over n x n'
+  double* rowpart;       // [CB][m]
+  double* colpart;       // [RB][m]
+  double* r; double* c;  // [m]
+  double* sig_part;      // [grid]
+  float* dlt_part;       // [grid]
+  double* mu_part;       // [grid]
+  float* rho_part;       // [grid]
+  DevIter* iter_out;     // this iteration's record
+  int* done;             // early-exit flag (converged / degenerate)
+};
+
+constexpr int kProjThreads = 256;
+constexpr int kProjTC = 512;  // columns per projection tile (32 lanes x float4 x 4 chunks)
+
+// host-side launchers (return cudaError_t)
+cudaError_t launch_proj(const ProjArgs& a, int grid, cudaStream_t s);
+int proj_max_grid(int device);
+cudaError_t launch_split(const float* src, int64_t lds, float* big, float* small, int64_t ldd,
+                         int rows, int cols, cudaStream_t s);
+cudaError_t launch_check_sym(const float* A, int64_t lda, int n, int* flags, cudaStream_t s);
+cudaError_t launch_check_finite(const float* A, int64_t lda, int rows, int cols, int* flags,
+                                cudaStream_t s);
+cudaError_t launch_fill(float* A, int64_t lda, int rows, int cols, float v, cudaStream_t s);
+cudaError_t launch_zero_slack(float* Y, int64_t ldY, int m, int n, int np, const int* done,
+                              cudaStream_t s);
+cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t ld, int rows,
+                        int cols, double* out2, cudaStream_t s);
+
+// GEMM: C[M x N] = P[M x K] * Q[N x K]^T (+ epilogue). Both operands K-major.
+enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2 };
+struct GemmArgs {
+  const float* P; int64_t ldP;     // plain fp32 operands (SIMT path)
+  const float* Q; int64_t ldQ;
+  const float* Pb; const float* Ps; // TF32 splits (tensor-core path), same ld as P
+  const float* Qb; const float* Qs; // same ld as Q
+  int M, N, K;
+  int epi;
+  float* C; int64_t ldC;           // plain output (or big part in kEpiSplit)
+  float* C2;                       // small part (kEpiSplit), ld = ldC
+  float* C3;                       // optional plain copy in kEpiSplit (nullable), ld = ldC
+  const float* D; int64_t ldD; float lam;  // kEpiAxpy: C = acc + lam * D
+  const int* done;                 // nullable early-exit flag
+};
+cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
+cudaError_t launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t s, int device);
+bool gemm_tc_supported(const GemmArgs& g);
+
+}  // namespace fpfp

@@ -1,0 +1,455 @@
+// proj.cu — the projection loop (Algorithm 1 lines 4-7) and the blend/rescale
+// (lines 8-9) as ONE persistent cooperative kernel per outer iteration.
+//
+// Y is the m x m slacked matrix. One sweep is P2(P1(Y)) with the closed forms
+//   P1(Y)_ij = Y_ij + (1 + sigma/m - r_i - c_j)/m,  r = Y 1, c = Y^T 1, sigma = 1^T Y 1  ({P1}, P:300-302
+//   with 1^T Y 1 as in Alg. 1 line 5, reading A2),   P2(Z) = (Z + |Z|)/2 = max(Z, 0)  ({P2})
+// and delta = max|Y_new - Y_old|. Every Z_ij needs the global sums of the previous Y,
+// so a sweep is: [tile pass: read Y, write Z, emit fp64 partial row/col sums of Z and a partial
+// delta] -> grid barrier -> [reduce partials to r, c, sigma] -> grid barrier. That is the minimum
+// of one HBM read + one HBM write of Y per sweep (DESIGN.md §Kernels "proj"). The sums of the
+// fresh GEMM output are taken by a read-only pass first. The inner loop (convergence test on
+// delta) runs on the device: every block computes the same delta from the same partials.
+//
+// Numerics: Y is stored in fp32; r, c, sigma and the P1 correction are
+// evaluated in fp64 (the first P1 after a GEMM cancels values ~1e2-1e3 down to O(1/m)), then the
+// result is rounded once to fp32. Reductions are two-stage with a fixed order (no float atomics),
+// so results are bitwise reproducible for a given grid.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fpfp {
+
+namespace {
+
+constexpr int kWarps = kProjThreads / kWarp;  // 8
+constexpr int kQ = kProjTC / 128;             // float4 chunks per lane per row (4)
+
+struct __align__(16) ProjSmem {
+  double col[kWarps][kProjTC];  // 32 KB: per-warp column partials of one tile
+  double red[kWarps];
+  double bcast[4];
+};
+
+// One tile pass over rows [rb*TR, ...) x cols [cb*512, ...) of Y.
+//   kSweep = false: sums only (Z = Y).   kSweep = true: Z = max(Y + t_i - u_j, 0), written back.
+template <bool kSweep>
+__device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double sigma, float& dmax,
+                                          ProjSmem& sm) {
+  const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = rb * p.TR;
+  const int row1 = min(p.m, row0 + p.TR);
+  const int colbase = cb * kProjTC;
+  const double inv_m = 1.0 / (double)p.m;
+
+  double u[kQ][4], colacc[kQ][4];
+  bool inrow[kQ];  // float4 inside the allocated row (col < ldY)
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int j0 = colbase + q * 128 + lane * 4;
+    inrow[q] = j0 < p.ldY;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = j0 + e;
+      u[q][e] = (kSweep && j < p.m) ? p.c[j] * inv_m : 0.0;
+      colacc[q][e] = 0.0;
+    }
+  }
+  const double tconst = (1.0 + sigma * inv_m) * inv_m;  // (1/n + 1^T Y 1 / n^2)
+
+  for (int i = row0 + warp; i < row1; i += kWarps) {
+    float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
+    float4 v[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+      v[q] = inrow[q] ? *reinterpret_cast<const float4*>(rowp + q * 128) : make_float4(0, 0, 0, 0);
+    const double ti = kSweep ? tconst - p.r[i] * inv_m : 0.0;
+    double racc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      float* ve = reinterpret_cast<float*>(&v[q]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = colbase + q * 128 + lane * 4 + e;
+        const bool valid = j < p.m;
+        const float y = ve[e];
+        float z = y;
+        if (kSweep) {
+          const double zd = ((double)y + ti) - u[q][e];          // P1, fp64
+          z = valid ? (float)fmax(zd, 0.0) : 0.0f;                // P2, one rounding to fp32
+          dmax = fmaxf(dmax, (float)fabs((double)z - (double)y)); // delta
+          ve[e] = z;
+        } else if (!valid) {
+          z = 0.0f;
+        }
+        racc += (double)z;
+        colacc[q][e] += (double)z;
+      }
+    }
+    if (kSweep) {
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        if (inrow[q]) *reinterpret_cast<float4*>(rowp + q * 128) = v[q];
+    }
+    racc = warp_sum(racc);
+    if (lane == 0) p.rowpart[(int64_t)cb * p.m + i] = racc;
+  }
+  // column partials of this tile: combine the 8 warps in a fixed order
+#pragma unroll
+  for (int q = 0; q < kQ; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm.col[warp][q * 128 + lane * 4 + e] = colacc[q][e];
+  __syncthreads();
+  for (int jj = threadIdx.x; jj < kProjTC; jj += kProjThreads) {
+    const int j = colbase + jj;
+    if (j < p.m) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += sm.col[w][jj];
+      p.colpart[(int64_t)rb * p.m + j] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// r_i = sum_cb rowpart[cb][i], c_j = sum_rb colpart[rb][j]; one warp per index: lane l sums the
+// partials l, l+32, ... and an xor tree combines the lanes (a fixed order => deterministic).
+// Per-block partial of sigma = sum of the c_j this block produced (fixed assignment of j to blocks).
+__device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  double local = 0.0;  // meaningful in lane 0
+  for (int j = gw; j < p.m; j += nw) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int rb = lane; rb < p.RB; rb += 32) s += p.colpart[(int64_t)rb * p.m + j];
+    s = warp_sum(s);
+    if (lane == 0) { p.c[j] = s; local += s; }
+  }
+  for (int i = gw; i < p.m; i += nw) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int cb = lane; cb < p.CB; cb += 32) s += p.rowpart[(int64_t)cb * p.m + i];
+    s = warp_sum(s);
+    if (lane == 0) p.r[i] = s;
+  }
+  if (lane == 0) sm.red[warp] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s += sm.red[w];
+    p.sig_part[blockIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// sigma = sum_b sig_part[b] (fixed order; identical in every block), broadcast through smem.
+__device__ __forceinline__ double grid_sigma(const ProjArgs& p, ProjSmem& sm) {
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += p.sig_part[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) sm.bcast[0] = s;
+  }
+  __syncthreads();
+  const double v = sm.bcast[0];
+  __syncthreads();
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_max(T v, ProjSmem& sm, T init) {
+  v = warp_max(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sm.red[warp] = (double)v;
+  __syncthreads();
+  T r = init;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kWarps; ++w) r = max(r, (T)sm.red[w]);
+    sm.bcast[1] = (double)r;
+  }
+  __syncthreads();
+  r = (T)sm.bcast[1];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T grid_max(const T* parts, ProjSmem& sm, T init) {
+  if (threadIdx.x < 32) {
+    T v = init;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) v = max(v, parts[b]);
+    v = warp_max(v);
+    if (threadIdx.x == 0) sm.bcast[2] = (double)v;
+  }
+  __syncthreads();
+  const T r = (T)sm.bcast[2];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
+  if (*p.done) return;  // an earlier iteration of this launch batch converged (uniform)
+  cg::grid_group grid = cg::this_grid();
+  __shared__ ProjSmem sm;
+  const int ntiles = p.RB * p.CB;
+  float dummy = 0.0f;
+
+  if (p.do_sums) {
+    // sums of the current Y (fresh GEMM block + retained slack)
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+  }
+  double sigma = grid_sigma(p, sm);
+
+  int sweeps = 0;
+  float delta = 0.0f;
+  for (;;) {
+    float dmax = 0.0f;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
+    dmax = block_max(dmax, sm, 0.0f);
+    if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+    sigma = grid_sigma(p, sm);
+    delta = grid_max(p.dlt_part, sm, 0.0f);
+    ++sweeps;
+    if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
+  }
+
+  if (!p.do_finalize) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.iter_out->valid = 1;
+      p.iter_out->sweeps = sweeps;
+      p.iter_out->delta = (double)delta;
+    }
+    return;
+  }
+
+  // ---- Algorithm 1 line 8: X~ = (1 - alpha) X + alpha Y[0:n, 0:n'];  line 9: X = X~ / max X~
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ftiles = p.RBx * p.CBx;
+  const double a = p.alpha, b = 1.0 - p.alpha;
+  double mu_loc = -INFINITY;
+  for (int t = blockIdx.x; t < ftiles; t += gridDim.x) {
+    const int rb = t / p.CBx, cb = t - (t / p.CBx) * p.CBx;
+    const int row1 = min(p.n, (rb + 1) * p.TR);
+    for (int i = rb * p.TR + warp; i < row1; i += kWarps) {
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int j0 = cb * kProjTC + q * 128 + lane * 4;
+        if (j0 >= p.np) continue;
+        const float4 xv = *reinterpret_cast<const float4*>(p.X + (int64_t)i * p.ldX + j0);
+        const float4 yv = *reinterpret_cast<const float4*>(p.Y + (int64_t)i * p.ldY + j0);
+        const float* xe = reinterpret_cast<const float*>(&xv);
+        const float* ye = reinterpret_cast<const float*>(&yv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (j0 + e < p.np) mu_loc = fmax(mu_loc, b * (double)xe[e] + a * (double)ye[e]);
+      }
+    }
+  }
+  mu_loc = block_max(mu_loc, sm, (double)-INFINITY);
+  if (threadIdx.x == 0) p.mu_part[blockIdx.x] = mu_loc;
+  grid.sync();
+  const double mu = grid_max(p.mu_part, sm, (double)-INFINITY);
+  if (!(mu > 1e-300)) {  // degenerate guard (reading A7): X left unchanged, loop stops
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->degenerate = 1;
+      p.iter_out->delta = (double)delta; p.iter_out->mu = mu; p.iter_out->rho = 0.0;
+      *p.done = 1;
+    }
+    return;
+  }
+  const double inv_scale = p.rescale ? mu : 1.0;
+  float rho_loc = 0.0f;
+  for (int t = blockIdx.x; t < ftiles; t += gridDim.x) {
+    const int rb = t / p.CBx, cb = t - (t / p.CBx) * p.CBx;
+    const int row1 = min(p.n, (rb + 1) * p.TR);
+    for (int i = rb * p.TR + warp; i < row1; i += kWarps) {
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int j0 = cb * kProjTC + q * 128 + lane * 4;
+        if (j0 >= p.np) continue;
+        float* xp = p.X + (int64_t)i * p.ldX + j0;
+        float4 xv = *reinterpret_cast<const float4*>(xp);
+        const float4 yv = *reinterpret_cast<const float4*>(p.Y + (int64_t)i * p.ldY + j0);
+        float* xe = reinterpret_cast<float*>(&xv);
+        const float* ye = reinterpret_cast<const float*>(&yv);
+        float4 bv, sv;
+        float* be = reinterpret_cast<float*>(&bv);
+        float* se = reinterpret_cast<float*>(&sv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float xn = 0.0f;
+          if (j0 + e < p.np) {
+            const double xt = b * (double)xe[e] + a * (double)ye[e];
+            xn = (float)(xt / inv_scale);
+            rho_loc = fmaxf(rho_loc, (float)fabs((double)xn - (double)xe[e]));
+          }
+          xe[e] = xn;
+          be[e] = tf32_rna(xn);
+          se[e] = tf32_rna(xn - be[e]);
+        }
+        *reinterpret_cast<float4*>(xp) = xv;
+        if (p.split) {
+          *reinterpret_cast<float4*>(p.Xb + (int64_t)i * p.ldX + j0) = bv;
+          *reinterpret_cast<float4*>(p.Xs + (int64_t)i * p.ldX + j0) = sv;
+        }
+      }
+    }
+  }
+  rho_loc = block_max(rho_loc, sm, 0.0f);
+  if (threadIdx.x == 0) p.rho_part[blockIdx.x] = rho_loc;
+  grid.sync();
+  if (blockIdx.x == 0) {
+    const float rho = grid_max(p.rho_part, sm, 0.0f);
+    if (threadIdx.x == 0) {
+      p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->degenerate = 0;
+      p.iter_out->delta = (double)delta; p.iter_out->mu = mu; p.iter_out->rho = (double)rho;
+      const int conv = (double)rho < p.eps1;
+      p.iter_out->converged = conv;
+      if (conv) *p.done = 1;
+    }
+  }
+}
+
+__global__ void split_kernel(const float* __restrict__ src, int64_t lds, float* __restrict__ big,
+                             float* __restrict__ small, int64_t ldd, int rows, int cols) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(k / cols), j = (int)(k - (k / cols) * cols);
+    const float a = src[(int64_t)i * lds + j];
+    const float hb = tf32_rna(a);
+    big[(int64_t)i * ldd + j] = hb;
+    small[(int64_t)i * ldd + j] = tf32_rna(a - hb);
+  }
+}
+
+__global__ void check_sym_kernel(const float* __restrict__ A, int64_t lda, int n, int* flags) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(k / n), j = (int)(k - (k / n) * n);
+    const float a = A[(int64_t)i * lda + j];
+    if (!isfinite(a)) atomicOr(flags, 2);
+    if (j > i && a != A[(int64_t)j * lda + i]) atomicOr(flags, 1);
+  }
+}
+
+__global__ void check_finite_kernel(const float* __restrict__ A, int64_t lda, int rows, int cols,
+                                    int* flags) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(k / cols), j = (int)(k - (k / cols) * cols);
+    if (!isfinite(A[(int64_t)i * lda + j])) atomicOr(flags, 2);
+  }
+}
+
+__global__ void fill_kernel(float* A, int64_t lda, int rows, int cols, float v) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(k / cols), j = (int)(k - (k / cols) * cols);
+    A[(int64_t)i * lda + j] = v;
+  }
+}
+
+// zero every entry of Y outside the X block [0:n, 0:n'] (slack_mode = reset)
+__global__ void zero_slack_kernel(float* Y, int64_t ldY, int m, int n, int np, const int* done) {
+  if (done && *done) return;
+  const int64_t total = (int64_t)m * m;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(k / m), j = (int)(k - (k / m) * m);
+    if (i >= n || j >= np) Y[(int64_t)i * ldY + j] = 0.0f;
+  }
+}
+
+// out2[0] = sum X∘G, out2[1] = sum X∘K  (fp64; single block so the order is fixed)
+__global__ void dot2_kernel(const float* X, const float* G, const float* K, int64_t ld, int rows,
+                            int cols, double* out2) {
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+    const int i = (int)(k / cols), j = (int)(k - (k / cols) * cols);
+    const double x = X[(int64_t)i * ld + j];
+    s0 += x * (double)G[(int64_t)i * ld + j];
+    if (K) s1 += x * (double)K[(int64_t)i * ld + j];
+  }
+  __shared__ double r0[32], r1[32];
+  s0 = warp_sum(s0); s1 = warp_sum(s1);
+  if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = s0; r1[threadIdx.x >> 5] = s1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += r0[w]; b += r1[w]; }
+    out2[0] = a; out2[1] = b;
+  }
+}
+
+inline int grid_for(int64_t total) {
+  return (int)std::min<int64_t>(4096, std::max<int64_t>(1, ceil_div(total, 256)));
+}
+
+}  // namespace
+
+int proj_max_grid(int device) {
+  int sms = 0, per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_kernel, kProjThreads, 0);
+  return sms * std::max(per_sm, 0);
+}
+
+cudaError_t launch_proj(const ProjArgs& a, int grid, cudaStream_t s) {
+  ProjArgs copy = a;
+  void* args[] = {&copy};
+  return cudaLaunchCooperativeKernel((void*)proj_kernel, dim3(grid), dim3(kProjThreads), args, 0, s);
+}
+
+cudaError_t launch_split(const float* src, int64_t lds, float* big, float* small, int64_t ldd,
+                         int rows, int cols, cudaStream_t s) {
+  split_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(src, lds, big, small, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_sym(const float* A, int64_t lda, int n, int* flags, cudaStream_t s) {
+  check_sym_kernel<<<grid_for((int64_t)n * n), 256, 0, s>>>(A, lda, n, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* A, int64_t lda, int rows, int cols, int* flags,
+                                cudaStream_t s) {
+  check_finite_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(A, lda, rows, cols, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(float* A, int64_t lda, int rows, int cols, float v, cudaStream_t s) {
+  fill_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(A, lda, rows, cols, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_slack(float* Y, int64_t ldY, int m, int n, int np, const int* done,
+                              cudaStream_t s) {
+  zero_slack_kernel<<<grid_for((int64_t)m * m), 256, 0, s>>>(Y, ldY, m, n, np, done);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t ld, int rows,
+                        int cols, double* out2, cudaStream_t s) {
+  dot2_kernel<<<1, 1024, 0, s>>>(X, G, K, ld, rows, cols, out2);
+  return cudaGetLastError();
+}
+
+}  // namespace fpfp

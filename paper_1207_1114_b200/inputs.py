@@ -211,6 +211,23 @@ def random_problem(seed: int, n: int, n_prime: int, d: int = 0, p: float = 0.5, 
                    eps2=eps2, max_iter1=max_iter1, max_iter2=max_iter2, seed=seed)
 
 
+def planted_unequal(seed: int, n: int, n_prime: int, d: int = 0, lam: float = 0.5,
+                    eps1: float = 1e-5, eps2: float = 1e-5, max_iter1: int = 25,
+                    max_iter2: int = 60) -> Problem:
+    """Small config-3-style pair (planted noisy subgraph + outliers) of any orientation: when
+    n > n' the roles of the two graphs are swapped (the larger graph carries the outliers)."""
+    small, big = min(n, n_prime), max(n, n_prime)
+    q = config3(seed=seed, n=small, n_prime=big, d=max(d, 1))
+    B, Bp = (q.B, q.Bp) if d > 0 else (None, None)
+    if n <= n_prime:
+        A, Ap = q.A, q.Ap
+    else:
+        A, Ap, B, Bp = q.Ap, q.A, Bp, B
+    return Problem(f"planted_{n}x{n_prime}_d{d}", A, Ap, B, Bp, lam=lam if d > 0 else 0.0,
+                   alpha=0.5, eps1=eps1, eps2=eps2, max_iter1=max_iter1, max_iter2=max_iter2,
+                   seed=seed)
+
+
 def random_matrix(seed: int, rows: int, cols: int, scale: float = 1.0, shift: float = 0.0) -> np.ndarray:
     """Plain seeded float32 matrix (e.g. a Y for one projection sweep)."""
     rng = np.random.Generator(np.random.PCG64(seed))
