@@ -95,7 +95,10 @@ typedef enum fastpfp_option {
   FASTPFP_OPT_CHECK_EVERY = 5,
   /* 1 = record CUDA events around every GEMM and projection launch on the handle's stream and
    * accumulate their device time into fastpfp_stats (bench.py's per-kernel roofline); 0 = off. */
-  FASTPFP_OPT_PROFILE = 6
+  FASTPFP_OPT_PROFILE = 6,
+  /* tensor-core GEMM tiling: 2 (default) = 256 x 256 tiles per CTA pair (tcgen05 cta_group::2),
+   * 1 = 128 x 128 tiles per CTA (cta_group::1). Same arithmetic, same results up to ordering. */
+  FASTPFP_OPT_GEMM_CTA_GROUP = 7
 } fastpfp_option;
 
 /* Counters of a handle (since creation or the last fastpfp_reset_stats). */
@@ -191,9 +194,10 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
                     double* delta_out, int64_t stream);
 
 /* C[M x N] = P[M x K] * Q[N x K]^T (both operands K-major, i.e. row-major with K contiguous) in
- * the given precision (FASTPFP_OPT_PRECISION values); the product behind A X A'. */
+ * the given precision (FASTPFP_OPT_PRECISION values) and tensor-core tiling cta_group (1 or 2,
+ * FASTPFP_OPT_GEMM_CTA_GROUP); the product behind A X A'. */
 int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
-                    int precision, int64_t stream);
+                    int precision, int cta_group, int64_t stream);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "fastpfp.h")
 
 OK, EINVAL, ESYM, ENONFINITE, ESTATE, ENOMEM, ECUDA, ENCCL, ENODEV, EPOISONED, EUNSUPPORTED = range(11)
 OPT_SLACK_MODE, OPT_PRECISION, OPT_RESCALE, OPT_STREAM, OPT_CHECK_EVERY, OPT_PROFILE = 1, 2, 3, 4, 5, 6
+OPT_GEMM_CTA_GROUP = 7
 PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT = 0, 1, 2
 
 
@@ -86,7 +87,7 @@ def lib():
         "fastpfp_abi_version": (C.c_int, []),
         "fastpfp_device_arch": (C.c_int, []),
         "fastpfp_project": (C.c_int, [FP, I64, D, I32, C.POINTER(I32), C.POINTER(D), I64]),
-        "fastpfp_gemm_nt": (C.c_int, [FP, FP, FP, I64, I64, I64, C.c_int, I64]),
+        "fastpfp_gemm_nt": (C.c_int, [FP, FP, FP, I64, I64, I64, C.c_int, C.c_int, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -257,10 +258,10 @@ def project(Y, eps2: float, max_iter2: int, stream: int = 0):
     return sweeps.value, delta.value
 
 
-def gemm_nt(P, Q, C_out, precision: int = PREC_TF32X3, stream: int = 0):
+def gemm_nt(P, Q, C_out, precision: int = PREC_TF32X3, cta_group: int = 2, stream: int = 0):
     """C = P Q^T on dense float32 CUDA tensors (fastpfp_gemm_nt)."""
     M, K = P.shape
     N = Q.shape[0]
     _check(lib().fastpfp_gemm_nt(P.data_ptr(), Q.data_ptr(), C_out.data_ptr(), M, N, K,
-                                 int(precision), int(stream)))
+                                 int(precision), int(cta_group), int(stream)))
     return C_out

@@ -49,7 +49,7 @@ struct fastpfp_handle {
   double* scal = nullptr;         // device scalars (objective)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int slack_mode = 0, precision = 2, rescale = 1, check_every = 4;
+  int slack_mode = 0, precision = 0, rescale = 1, check_every = 4, cta_group = 2;
   bool graphs_set = false, x0_custom = false, poisoned = false;
   int64_t t = 0;
   std::string err;
@@ -150,6 +150,7 @@ int run_gemm(fastpfp_handle* h, GemmArgs& g) {
   cudaError_t e;
   h->stats.launches += 1;
   h->stats.gemm_launches += 1;
+  g.cta_group = h->cta_group;
   if (h->precision == 2 || !gemm_tc_supported(g)) {
     if (h->precision != 2)
       return set_err(h, FASTPFP_EUNSUPPORTED, "tensor-core GEMM does not support M=%d N=%d K=%d",
@@ -316,6 +317,9 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
     case FASTPFP_OPT_CHECK_EVERY:
       if (value < 1 || value > kMaxCheck) return FASTPFP_EINVAL;
       h->check_every = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_GEMM_CTA_GROUP:
+      if (value != 1 && value != 2) return FASTPFP_EINVAL;
+      h->cta_group = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_PROFILE:
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
       if (value && !h->ev_ready) {
@@ -417,7 +421,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
       g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
       g1.M = NP; g1.N = N; g1.K = NP;
-      g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.C3 = h->U.p; g1.ldC = h->U.ld;
+      g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->U.ld;
+      g1.C3 = h->precision == 2 ? h->U.p : nullptr;   // plain U only feeds the SIMT GEMM2
       g1.done = h->done;
       int rc = run_gemm(h, g1);
       if (rc) return rc;
@@ -533,7 +538,8 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
   g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
   g1.M = NP; g1.N = N; g1.K = NP;
-  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.C3 = h->U.p; g1.ldC = h->U.ld;
+  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->U.ld;
+  g1.C3 = h->precision == 2 ? h->U.p : nullptr;
   int rc = run_gemm(h, g1);
   if (rc) return rc;
   GemmArgs g2{};
@@ -610,8 +616,9 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
 }
 
 int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
-                    int precision, int64_t stream) {
-  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || precision < 0 || precision > 2)
+                    int precision, int cta_group, int64_t stream) {
+  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || precision < 0 || precision > 2 ||
+      (cta_group != 1 && cta_group != 2))
     return FASTPFP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int dev = 0;
@@ -630,6 +637,7 @@ int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t
     g.P = Pp.p; g.ldP = Pp.ld; g.Pb = Pb.p; g.Ps = Ps.p;
     g.Q = Qp.p; g.ldQ = Qp.ld; g.Qb = Qb.p; g.Qs = Qs.p;
     g.M = (int)M; g.N = (int)N; g.K = (int)K; g.epi = kEpiPlain; g.C = Cp.p; g.ldC = Cp.ld;
+    g.cta_group = cta_group;
     if (precision == 2) {
       A(launch_gemm_simt(g, s));
     } else if (!gemm_tc_supported(g)) {

@@ -96,6 +96,7 @@ struct GemmArgs {
   float* C3;                       // optional plain copy in kEpiSplit (nullable), ld = ldC
   const float* D; int64_t ldD; float lam;  // kEpiAxpy: C = acc + lam * D
   const int* done;                 // nullable early-exit flag
+  int cta_group = 2;               // tensor-core path: 1 = 128x128 tiles per CTA, 2 = 256x256 per CTA pair
 };
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t s, int device);

@@ -33,10 +33,12 @@ class PairResult:
     X_oracle: np.ndarray
 
 
-def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=None):
-    from paper_1207_1114_b200 import OPT_CHECK_EVERY, OPT_PRECISION, OPT_RESCALE, OPT_SLACK_MODE, Solver
+def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=None, cta_group=2):
+    from paper_1207_1114_b200 import (OPT_CHECK_EVERY, OPT_GEMM_CTA_GROUP, OPT_PRECISION, OPT_RESCALE,
+                                      OPT_SLACK_MODE, Solver)
     s = Solver(p.n, p.n_prime, p.d)
     s.set_option(OPT_PRECISION, precision)
+    s.set_option(OPT_GEMM_CTA_GROUP, cta_group)
     s.set_option(OPT_SLACK_MODE, slack_mode)
     s.set_option(OPT_RESCALE, rescale)
     if check_every:

@@ -59,16 +59,20 @@ def test_sweeps_vs_oracle(m):
         assert abs(d - do) <= 2e-6 * max(1.0, np.max(np.abs(Y0)))
 
 
-@pytest.mark.parametrize("prec", PRECS)
+GEMM_VARIANTS = [pytest.param(0, 2, id="tf32x3-cg2"), pytest.param(0, 1, id="tf32x3-cg1"),
+                 pytest.param(2, 2, id="simt")]
+
+
+@pytest.mark.parametrize("prec,cg", GEMM_VARIANTS)
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (129, 257, 33), (300, 1000, 700),
-                                   (1000, 1000, 1000), (256, 512, 4096)])
-def test_gemm_nt_error_bound(prec, M, N, K):
+                                   (1000, 1000, 1000), (256, 512, 4096), (1500, 700, 2048)])
+def test_gemm_nt_error_bound(prec, cg, M, N, K):
     import paper_1207_1114_b200 as F
     r = np.random.default_rng(M * 7 + N * 3 + K)
     P = r.random((M, K), dtype=np.float32) * (r.random((M, K)) < 0.5)
     Q = r.random((N, K), dtype=np.float32)
     C = torch.empty((M, N), dtype=torch.float32, device="cuda")
-    F.gemm_nt(torch.from_numpy(P.astype(np.float32)).cuda(), torch.from_numpy(Q).cuda(), C, prec)
+    F.gemm_nt(torch.from_numpy(P.astype(np.float32)).cuda(), torch.from_numpy(Q).cuda(), C, prec, cg)
     exact = P.astype(np.float64) @ Q.astype(np.float64).T
     mag = np.abs(P.astype(np.float64)) @ np.abs(Q.astype(np.float64)).T
     # fp32 accumulation: |err| <= K u |P||Q|^T (u = 2^-24); 3xTF32 adds <= 3 * 2^-22 |P||Q|^T
@@ -157,13 +161,14 @@ def test_config3_unequal_outliers(prec):
     assert_parity(res)
 
 
-@pytest.mark.parametrize("prec", PRECS)
-def test_config5_recipe_reduced(prec):
-    # the c5 recipe (p = 0.1, d = 64, lambda = 1, fixed 20 x 20) at n = 2048: spans 4 x 16 GEMM tiles,
-    # 4 x 16 projection tile columns, exercised by the oracle in seconds
+@pytest.mark.parametrize("prec,cg", [pytest.param(0, 2, id="tf32x3"), pytest.param(0, 1, id="tf32x3-cg1"),
+                                     pytest.param(2, 2, id="simt")])
+def test_config5_recipe_reduced(prec, cg):
+    # the c5 recipe (p = 0.1, d = 64, lambda = 1, fixed 20 x 20) at n = 2048: spans 8 x 8 pair tiles
+    # of the GEMM and 4 x 16 projection tile columns, exercised by the oracle in seconds
     p = inputs.config5(n=2048)
     p.max_iter1 = 6
-    res = run_pair(p, prec, lockstep=6)
+    res = run_pair(p, prec, lockstep=6, cta_group=cg)
     assert max(res.lockstep_max) <= 1e-4 and res.final_diff <= 1e-4
     assert res.gpu_sweeps == res.oracle_sweeps == [20] * 6
 
@@ -171,6 +176,20 @@ def test_config5_recipe_reduced(prec):
 # ---------------------------------------------------------------------------------------------
 # contract details
 # ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_tf32_single_pass_error_is_tf32_sized(cg):
+    # plain 1xTF32 (reported separately, not parity-accurate): error ~ 2^-11 relative per operand
+    import paper_1207_1114_b200 as F
+    r = np.random.default_rng(3)
+    M, N, K = 384, 640, 1024
+    P = r.random((M, K), dtype=np.float32); Q = r.random((N, K), dtype=np.float32)
+    C = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    F.gemm_nt(torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda(), C, F.PREC_TF32, cg)
+    exact = P.astype(np.float64) @ Q.astype(np.float64).T
+    rel = np.max(np.abs(C.cpu().numpy() - exact) / exact)
+    assert 1e-7 < rel < 2.0**-9
+
 
 def test_k_single_steps_equal_one_call_bitwise():
     import paper_1207_1114_b200 as F
