@@ -182,6 +182,42 @@ int fastpfp_abi_version(void);
 int fastpfp_device_arch(void);
 
 /* ---------------------------------------------------------------------------------------------
+ * Batches of small pairs (BASELINE configs[3]: 8192 independent pairs of n = n' = 128)
+ *
+ * Every pair runs the whole of Algorithm 1 inside one CTA, on chip, with its own
+ * convergence; the same scalars (alpha, lambda, eps, maxIter) apply to all pairs.
+ * Arrays are pair-major and dense: A [batch][n][n], A' [batch][n'][n'], B [batch][n][d],
+ * B' [batch][n'][d], X [batch][n][n']. Limits: 1 <= n, n' <= 128. Projection arithmetic is fp32
+ * here; products are fp32 FFMA. Multi-GPU: pairs are split across ranks by the
+ * caller (one handle per GPU, no communication, BASELINE configs[3] "pairs split evenly").
+ * ------------------------------------------------------------------------------------------- */
+typedef struct fastpfp_batched fastpfp_batched;
+
+/* Errors: EINVAL (batch < 1, sizes outside [1,128], d < 0), ENODEV, ENOMEM. */
+int fastpfp_batched_create(int64_t batch, int64_t n, int64_t n_prime, int64_t d,
+                           fastpfp_batched** out);
+/* Load all pairs (copied; ESYM / ENONFINITE as fastpfp_set_graphs); K = B B'^T per pair;
+ * resets every pair to X0 (default 1 1^T/(n n')) and zero slack. */
+int fastpfp_batched_set_graphs(fastpfp_batched* h, const float* A, const float* A_prime,
+                               const float* B, const float* B_prime, int is_device);
+/* X0 [batch][n][n'] (NULL: 1 1^T/(n n') for every pair); resets all pairs. */
+int fastpfp_batched_set_x0(fastpfp_batched* h, const float* X0, int is_device);
+/* Up to max_iter1 outer iterations per pair, continuing from each pair's state. Per-pair outputs
+ * (host arrays of length batch, each nullable): iterations done, converged flag, sweeps made. */
+int fastpfp_batched_iterate(fastpfp_batched* h, double alpha, double lambda, double eps1,
+                            double eps2, int32_t max_iter1, int32_t max_iter2, float* X_out,
+                            int32_t* iterations, int32_t* converged, int32_t* sweeps);
+/* Current X of all pairs to dst ([batch][n][n'], host or device). */
+int fastpfp_batched_copy_x(fastpfp_batched* h, float* dst, int dst_is_device);
+/* Greedy discretization (ties: smaller row, then column) of every pair on the device:
+ * assign [batch][n] (host), assign[p*n + i] = column or -1. */
+int fastpfp_batched_discretize(fastpfp_batched* h, int32_t* assign);
+int fastpfp_batched_set_option(fastpfp_batched* h, int key, int64_t value); /* STREAM, RESCALE */
+int fastpfp_batched_get_stats(fastpfp_batched* h, fastpfp_stats* out);
+void fastpfp_batched_destroy(fastpfp_batched* h);
+const char* fastpfp_batched_last_error(const fastpfp_batched* h);
+
+/* ---------------------------------------------------------------------------------------------
  * Building blocks (exposed for unit parity tests; same kernels the iterate path launches).
  * All pointers are DEVICE pointers, dense row-major float32 unless stated; stream 0 = default.
  * ------------------------------------------------------------------------------------------- */

@@ -87,6 +87,16 @@ def lib():
         "fastpfp_abi_version": (C.c_int, []),
         "fastpfp_device_arch": (C.c_int, []),
         "fastpfp_project": (C.c_int, [FP, I64, D, I32, C.POINTER(I32), C.POINTER(D), I64]),
+        "fastpfp_batched_create": (C.c_int, [I64, I64, I64, I64, C.POINTER(H)]),
+        "fastpfp_batched_set_graphs": (C.c_int, [H, FP, FP, FP, FP, C.c_int]),
+        "fastpfp_batched_set_x0": (C.c_int, [H, FP, C.c_int]),
+        "fastpfp_batched_iterate": (C.c_int, [H, D, D, D, D, I32, I32, FP, VP, VP, VP]),
+        "fastpfp_batched_copy_x": (C.c_int, [H, FP, C.c_int]),
+        "fastpfp_batched_discretize": (C.c_int, [H, VP]),
+        "fastpfp_batched_set_option": (C.c_int, [H, C.c_int, I64]),
+        "fastpfp_batched_get_stats": (C.c_int, [H, C.POINTER(Stats)]),
+        "fastpfp_batched_destroy": (None, [H]),
+        "fastpfp_batched_last_error": (C.c_char_p, [H]),
         "fastpfp_gemm_nt": (C.c_int, [FP, FP, FP, I64, I64, I64, C.c_int, C.c_int, I64]),
     }
     for name, (res, args) in sig.items():
@@ -111,10 +121,10 @@ def _ptr(x):
     return a.ctypes.data, 0, a
 
 
-def _check(st: int, h=None):
+def _check(st: int, h=None, err_fn="fastpfp_last_error"):
     if st != OK:
         L = lib()
-        msg = (L.fastpfp_last_error(h) or b"").decode() if h else ""
+        msg = (getattr(L, err_fn)(h) or b"").decode() if h else ""
         raise FastPFPError(st, f"{L.fastpfp_status_string(st).decode()}: {msg}")
 
 
@@ -265,3 +275,84 @@ def gemm_nt(P, Q, C_out, precision: int = PREC_TF32X3, cta_group: int = 2, strea
     _check(lib().fastpfp_gemm_nt(P.data_ptr(), Q.data_ptr(), C_out.data_ptr(), M, N, K,
                                  int(precision), int(cta_group), int(stream)))
     return C_out
+
+
+@dataclass
+class BatchReport:
+    iterations: np.ndarray
+    converged: np.ndarray
+    sweeps: np.ndarray
+
+
+class BatchedSolver:
+    """Many independent small pairs (n, n' <= 128), one CTA per pair (fastpfp_batched_*)."""
+
+    def __init__(self, batch: int, n: int, n_prime: int, d: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.fastpfp_batched_create(batch, n, n_prime, d, C.byref(h)))
+        self._h = h
+        self.batch, self.n, self.n_prime, self.d = batch, n, n_prime, d
+
+    def _ck(self, st):
+        _check(st, self._h, "fastpfp_batched_last_error")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().fastpfp_batched_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, key: int, value: int):
+        self._ck(lib().fastpfp_batched_set_option(self._h, key, int(value)))
+
+    def set_graphs(self, A, Ap, B=None, Bp=None):
+        pa, da, ka = _ptr(A)
+        pp, dp, kp = _ptr(Ap)
+        pb, db, kb = _ptr(B)
+        pbp, dbp, kbp = _ptr(Bp)
+        Solver._check_shape(A, (self.batch, self.n, self.n))
+        Solver._check_shape(Ap, (self.batch, self.n_prime, self.n_prime))
+        if self.d > 0:
+            Solver._check_shape(B, (self.batch, self.n, self.d))
+            Solver._check_shape(Bp, (self.batch, self.n_prime, self.d))
+        self._ck(lib().fastpfp_batched_set_graphs(self._h, pa, pp, pb, pbp, da))
+
+    def set_x0(self, X0=None):
+        p, dev, keep = _ptr(X0)
+        if X0 is not None:
+            Solver._check_shape(X0, (self.batch, self.n, self.n_prime))
+        self._ck(lib().fastpfp_batched_set_x0(self._h, p, dev))
+
+    def iterate(self, alpha, lam, eps1, eps2, max_iter1, max_iter2, want_x=True):
+        it = np.zeros(self.batch, np.int32)
+        cv = np.zeros(self.batch, np.int32)
+        sw = np.zeros(self.batch, np.int32)
+        X = np.empty((self.batch, self.n, self.n_prime), np.float32) if want_x else None
+        self._ck(lib().fastpfp_batched_iterate(self._h, float(alpha), float(lam), float(eps1),
+                                               float(eps2), int(max_iter1), int(max_iter2),
+                                               X.ctypes.data if X is not None else None,
+                                               it.ctypes.data, cv.ctypes.data, sw.ctypes.data))
+        return X, BatchReport(it, cv.astype(bool), sw)
+
+    def copy_x(self, out=None):
+        if out is None:
+            out = np.empty((self.batch, self.n, self.n_prime), np.float32)
+        p, dev, keep = _ptr(out) if hasattr(out, "data_ptr") else (out.ctypes.data, 0, out)
+        self._ck(lib().fastpfp_batched_copy_x(self._h, p, dev))
+        return out
+
+    def discretize(self):
+        out = np.empty((self.batch, self.n), np.int32)
+        self._ck(lib().fastpfp_batched_discretize(self._h, out.ctypes.data))
+        return out
+
+    def stats(self) -> dict:
+        st = Stats()
+        self._ck(lib().fastpfp_batched_get_stats(self._h, C.byref(st)))
+        return {k: getattr(st, k) for k, _ in Stats._fields_}

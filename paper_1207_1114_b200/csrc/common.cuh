@@ -98,6 +98,27 @@ struct GemmArgs {
   const int* done;                 // nullable early-exit flag
   int cta_group = 2;               // tensor-core path: 1 = 128x128 tiles per CTA, 2 = 256x256 per CTA pair
 };
+// Batched small-pair whole solve (small_solve.cu), n, n' <= 128, one pair per CTA.
+struct SmallArgs {
+  int batch, n, np, m;
+  const float* A;   // [batch][n][n]
+  const float* Ap;  // [batch][np][np]
+  const float* K;   // [batch][n][np] or null
+  float* X;         // [batch][n][np] state
+  float* Y;         // [batch][m][m] slack state (null when n == np)
+  float alpha, lam, eps1, eps2;
+  int max_iter1, max_iter2, rescale;
+  int32_t* iters;   // [batch] outer iterations done by this call
+  int32_t* conv;    // [batch]
+  int32_t* sweeps;  // [batch] total sweeps
+  float* rho;       // [batch] last rho
+  int32_t* degen;   // [batch]
+};
+size_t small_smem_bytes();
+cudaError_t launch_small_solve(const SmallArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_small_greedy(const float* X, int batch, int n, int np, int32_t* assign, int grid,
+                                cudaStream_t s);
+
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t s, int device);
 bool gemm_tc_supported(const GemmArgs& g);

@@ -236,3 +236,14 @@ def random_matrix(seed: int, rows: int, cols: int, scale: float = 1.0, shift: fl
 
 
 CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}
+
+
+def stack_pairs(problems):
+    """Pair-major dense arrays (A [b][n][n], A' [b][n'][n'], B, B') for the batched path."""
+    A = np.ascontiguousarray(np.stack([p.A for p in problems]))
+    Ap = np.ascontiguousarray(np.stack([p.Ap for p in problems]))
+    B = Bp = None
+    if problems[0].B is not None:
+        B = np.ascontiguousarray(np.stack([p.B for p in problems]))
+        Bp = np.ascontiguousarray(np.stack([p.Bp for p in problems]))
+    return A, Ap, B, Bp

@@ -1,0 +1,104 @@
+"""GPU parity of the batched small-pair path (BASELINE configs[3]; configs[0] as a batch of one)
+against the fp64 oracle, pair by pair, on the same seeded inputs (BJ tolerances)."""
+import numpy as np
+import pytest
+
+from oracle import fastpfp as O
+from paper_1207_1114_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1207_1114_b200 as F
+    F.lib()
+
+
+def _solve_batch(problems, max_iter1=None, x0=None):
+    import paper_1207_1114_b200 as F
+    p0 = problems[0]
+    s = F.BatchedSolver(len(problems), p0.n, p0.n_prime, p0.d)
+    s.set_graphs(*inputs.stack_pairs(problems))
+    if x0 is not None:
+        s.set_x0(x0)
+    X, rep = s.iterate(p0.alpha, p0.lam, p0.eps1, p0.eps2, max_iter1 or p0.max_iter1, p0.max_iter2)
+    return s, X, rep
+
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_config4_pairs_vs_oracle(fixed):
+    probs = inputs.config4(fixed=fixed, first=0, count=24)
+    s, X, rep = _solve_batch(probs)
+    assign = s.discretize()
+    for k, p in enumerate(probs):
+        Xo, ro, st = O.solve(p)
+        assert np.max(np.abs(X[k].astype(np.float64) - Xo)) <= 1e-4
+        assert abs(int(rep.iterations[k]) - ro.iterations) <= 1
+        if fixed:
+            assert rep.iterations[k] == 20 and rep.sweeps[k] == 400
+        ao = O.greedy_discretize(Xo)
+        assert np.array_equal(assign[k], ao)
+        assert np.array_equal(assign[k], p.perm)          # planted permutation recovered
+
+
+def test_config4_lockstep_first_10():
+    import paper_1207_1114_b200 as F
+    probs = inputs.config4(fixed=False, first=100, count=8)
+    p0 = probs[0]
+    s = F.BatchedSolver(len(probs), p0.n, p0.n_prime, 0)
+    s.set_graphs(*inputs.stack_pairs(probs))
+    states = [O.FastPFP(p.A, p.Ap) for p in probs]
+    for t in range(10):
+        X, rep = s.iterate(p0.alpha, p0.lam, 0.0, p0.eps2, 1, p0.max_iter2)
+        for k, st in enumerate(states):
+            Xo, _ = st.iterate(p0.lam, p0.alpha, 0.0, p0.eps2, 1, p0.max_iter2)
+            assert np.max(np.abs(X[k].astype(np.float64) - Xo)) <= 1e-4, (t, k)
+
+
+def test_config1_as_batch_of_one():
+    p = inputs.config1()
+    s, X, rep = _solve_batch([p], x0=p.X0[None])
+    Xo, ro, st = O.solve(p)
+    assert np.max(np.abs(X[0].astype(np.float64) - Xo)) <= 1e-4
+    assert abs(int(rep.iterations[0]) - ro.iterations) <= 1
+    assert np.array_equal(s.discretize()[0], p.perm)
+
+
+@pytest.mark.parametrize("shape", [(37, 53, 3), (53, 37, 3), (128, 100, 5), (1, 7, 2), (5, 1, 0)])
+def test_ragged_batched(shape):
+    n, npr, d = shape
+    probs = [inputs.planted_unequal(200 + k + n, n, npr, d=d, max_iter1=20) for k in range(3)]
+    s, X, rep = _solve_batch(probs)
+    for k, p in enumerate(probs):
+        Xo, ro, st = O.solve(p)
+        assert np.max(np.abs(X[k].astype(np.float64) - Xo)) <= 1e-4, k
+        assert np.array_equal(s.discretize()[k], O.greedy_discretize(Xo))
+
+
+def test_batched_greedy_matches_oracle_with_ties():
+    import paper_1207_1114_b200 as F
+    r = np.random.default_rng(4)
+    b, n, npr = 16, 20, 13
+    X0 = (np.round(r.random((b, n, npr)) * 3) / 3).astype(np.float32)   # many ties
+    s = F.BatchedSolver(b, n, npr, 0)
+    s.set_graphs(np.zeros((b, n, n), np.float32), np.zeros((b, npr, npr), np.float32))
+    s.set_x0(X0)
+    a = s.discretize()
+    for k in range(b):
+        assert np.array_equal(a[k], O.greedy_discretize(X0[k].astype(np.float64)))
+
+
+def test_batched_k_steps_equal_one_call():
+    probs = inputs.config4(fixed=True, first=7, count=4)
+    import paper_1207_1114_b200 as F
+    p0 = probs[0]
+    a = F.BatchedSolver(4, 128, 128, 0); a.set_graphs(*inputs.stack_pairs(probs))
+    Xa, _ = a.iterate(0.5, 0.0, 0.0, 0.0, 5, 20)
+    b = F.BatchedSolver(4, 128, 128, 0); b.set_graphs(*inputs.stack_pairs(probs))
+    for _ in range(5):
+        Xb, _ = b.iterate(0.5, 0.0, 0.0, 0.0, 1, 20)
+    assert np.array_equal(Xa, Xb)
