@@ -190,6 +190,7 @@ def run_ours(args):
     import torch
 
     import paper_1207_1114_b200 as F
+    from paper_1207_1114_b200 import dist as D
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -199,13 +200,23 @@ def run_ours(args):
 
     p = make_problem(args.workload)
     inner = p.max_iter2 if args.workload == "c5" else 20
-    s = F.Solver(p.n, p.n_prime, p.d)
+    sharded = world > 1 and args.workload == "c5"
+    if sharded:
+        # row-sharded pair (BASELINE configs[4]): this rank owns n/P rows; NCCL over NVLink
+        shard = D.row_partition(p.n, p.n_prime, world, rank)
+        s = D.make_solver(p.n, p.n_prime, p.d)
+        A_l, Ap_l, B_l, Bp_l = D.local_inputs(p, shard)
+    else:
+        shard = None
+        s = F.Solver(p.n, p.n_prime, p.d)
+        A_l, Ap_l, B_l, Bp_l = p.A, p.Ap, p.B, p.Bp
     stream = torch.cuda.current_stream()
     s.set_option(F.OPT_STREAM, stream.cuda_stream)
     s.set_option(F.OPT_PRECISION, prec)
     s.set_option(F.OPT_CHECK_EVERY, 64)
-    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
-    s.set_x0(p.X0)
+    s.set_graphs(A_l, Ap_l, B_l, Bp_l)
+    if p.X0 is not None:
+        s.set_x0(p.X0 if not sharded else np.ascontiguousarray(p.X0[shard.sl]))
 
     # warm-up (untimed)
     s.iterate(p.alpha, p.lam, 0.0, 0.0, max(args.warmup, 1), inner, want_x=False)
@@ -235,7 +246,8 @@ def run_ours(args):
         ms, clocks, st = timed()   # rejected run (thermal / hw slowdown): re-measure once
         clocks["remeasured"] = True
     ms_max = max_over_ranks(ms, world)
-    value = args.steps * world / (ms_max / 1e3)      # replicas: every rank runs its own pair
+    # sharded: the ranks cooperate on ONE pair (strong scaling); else every rank runs its own pair
+    value = args.steps / (ms_max / 1e3) if sharded else args.steps * world / (ms_max / 1e3)
 
     # roofline of the dominant kernel (the GEMM at c5; one kernel, two launches per step)
     gemm_ms = st["gemm_ms"] / max(st["gemm_launches"], 1)
@@ -243,7 +255,8 @@ def run_ours(args):
     achieved_tf = flops_launch / (gemm_ms / 1e3) / 1e12
     peak, bound, peak_note = gemm_peak(mp, src, prec)
     proj_ms = st["proj_ms"] / max(st["proj_launches"], 1)
-    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner)
+    rows_local = shard.rows if sharded else p.n
+    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner) * rows_local // p.n
     proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
     step_ms = ms / args.steps
     roofline = {
@@ -252,6 +265,8 @@ def run_ours(args):
         "traffic": ncu_traffic(f"gemm_{precision_name(prec)}"),
         "flops_per_launch": flops_launch, "ms_per_launch": round(gemm_ms, 4),
         "share_of_step": round(2 * gemm_ms / step_ms, 4), "peak_source": peak_note,
+        "note": ("gemm_ms spans both GEMM launches and, when sharded, the NCCL all-gather between them"
+                 if sharded else "per GEMM launch (GEMM1 and GEMM2 have equal flops at n = n')"),
         "secondary": {
             "kernel": "proj_kernel (sums + 20 sweeps + finalize)", "bound": "hbm",
             "achieved": round(proj_gbs, 1), "peak": mp["hbm_gbs"], "unit": "GB/s",
@@ -263,10 +278,11 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(p, args.workload), "n": p.n, "n_prime": p.n_prime, "d": p.d,
                    "inner_sweeps": inner, "gemm": precision_name(prec),
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": (f"rowshard{world} (NCCL all-gather of U + per-sweep all-reduce)" if sharded
+                                   else ("replicas" if world > 1 else "single")),
                    "l2": "inputs larger than L2 (A, A', Y 1.07 GB each vs 126 MB L2); no flush needed"
                    if args.workload == "c5" else "working set L2-resident"},
         "roofline": roofline, "clocks": clocks, "gpu_launches": int(st["launches"]),
@@ -275,7 +291,7 @@ def run_ours(args):
     # end to end through the public API with HOST buffers (pinned): upload graphs, full 20 x 20
     # solve, read X back
     if not args.no_e2e:
-        out["e2e"] = e2e(s, p, inner, stream, world)
+        out["e2e"] = e2e(s, p, inner, stream, world, shard)
     if rank == 0 and world == 1 and args.workload == "c5" and not args.no_secondary:
         out["secondary"] = secondary_c2(prec)
         out["secondary_c4"] = secondary_c4()
@@ -286,19 +302,24 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
 
 
-def e2e(s, p, inner, stream, world):
+def e2e(s, p, inner, stream, world, shard=None):
     import torch
-    pin = lambda a: torch.from_numpy(a).pin_memory() if a is not None else None
-    A, Ap, B, Bp = pin(p.A), pin(p.Ap), pin(p.B), pin(p.Bp)
-    Xh = torch.empty((p.n, p.n_prime), dtype=torch.float32).pin_memory()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() if a is not None else None
+    rows = p.n if shard is None else shard.rows
+    sl = slice(0, p.n) if shard is None else shard.sl
+    A, Ap = pin(p.A[sl]), pin(p.Ap)
+    B = pin(p.B[sl]) if p.B is not None else None
+    Bp = pin(p.Bp)
+    Xh = torch.empty((rows, p.n_prime), dtype=torch.float32).pin_memory()
     outer = p.max_iter1 if p.eps1 == 0.0 else 20
 
     def one():
         s.set_graphs(A, Ap, B, Bp)      # H2D from pinned host memory + validation + K = BB'^T
-        s.set_x0(p.X0)
+        s.set_x0(None if p.X0 is None else np.ascontiguousarray(p.X0[sl]))
         s.iterate(p.alpha, p.lam, 0.0, 0.0, outer, inner, want_x=False)
         s.copy_x(Xh)                    # D2H of the result
     one()                               # warm-up
@@ -313,8 +334,9 @@ def e2e(s, p, inner, stream, world):
     wall = time.perf_counter() - t0
     ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3), world)
     h2d = sum(x.numel() * 4 for x in (A, Ap, B, Bp) if x is not None)
-    return {"value": round(outer * world / (ms / 1e3), 4), "unit": UNIT,
-            "h2d_bytes_per_step": h2d // outer, "d2h_bytes_per_step": (p.n * p.n_prime * 4) // outer,
+    per_rank_pairs = 1 if shard is not None else world
+    return {"value": round(outer * per_rank_pairs / (ms / 1e3), 4), "unit": UNIT,
+            "h2d_bytes_per_step": h2d // outer, "d2h_bytes_per_step": (rows * p.n_prime * 4) // outer,
             "what": f"fastpfp_set_graphs(pinned host A,A',B,B') + set_x0 + iterate({outer} outer x {inner} sweeps) "
                     f"+ fastpfp_copy_x(pinned host); bytes amortised over the {outer} outer steps of one solve",
             "ms_per_solve": round(ms, 3)}

@@ -161,6 +161,30 @@ int fastpfp_discretize(fastpfp_handle* h, int32_t* assign);
  * fp64 over fp32 products. */
 int fastpfp_objective(fastpfp_handle* h, double lambda, double* f);
 
+/* ---------------------------------------------------------------------------------------------
+ * Row-sharded single pair over P GPUs of one node (BASELINE configs[4], one process per GPU)
+ *
+ * Rank r owns rows [r n/P, (r+1) n/P) of A, X, K, B and Y; A' and B' are replicated. Per outer
+ * iteration: GEMM1 U_r = A' X_r^T locally; NCCL all-gather of U's TF32 parts over NVLink;
+ * GEMM2 Y_r = A_r U^T + lambda K_r with a K-loop over the gathered rank blocks; per sweep an NCCL
+ * all-reduce (SUM) of the m column sums and sigma (row sums are local); all-reduce (MAX) of mu
+ * and rho. Requirements: n >= n', n % P == 0, (n/P) % 32 == 0 (else
+ * EUNSUPPORTED); tensor-core precision (0 or 1).
+ * On a sharded handle: fastpfp_set_graphs takes the LOCAL rows of A (n/P x n, row-major) and of B
+ * (n/P x d) and the full A' and B' (A's symmetry is the caller's contract; finiteness is checked);
+ * set_x0 / iterate's X_out / copy_x use the local rows of X (n/P x n'); fastpfp_discretize gathers
+ * X and returns the full assignment (length n) on every rank; fastpfp_objective returns the global
+ * f on every rank. All ranks must make the same calls in the same order (collectives).
+ * ------------------------------------------------------------------------------------------- */
+
+/* Write a fresh NCCL unique id (128 bytes) to out (call on rank 0; broadcast it to all ranks,
+ * e.g. over the torch process group). Errors: EINVAL (size < 128), ENCCL (NCCL not loadable). */
+int fastpfp_nccl_unique_id(void* out, int64_t size);
+
+/* Collective: every rank calls it with the same n, n', d, world and id. */
+int fastpfp_create_dist(int64_t n, int64_t n_prime, int64_t d, int rank, int world,
+                        const void* nccl_id, fastpfp_handle** out);
+
 /* Set an option (fastpfp_option). Errors: EINVAL for unknown keys or values. */
 int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value);
 

@@ -58,11 +58,27 @@ def declared_symbols() -> List[str]:
                                  src, flags=re.M)))
 
 
+def _nccl_hint():
+    """Point the library's NCCL loader at torch's bundled libnccl (the one the process uses)."""
+    if os.environ.get("FASTPFP_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as nv
+        for base in list(getattr(nv, "__path__", [])):
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["FASTPFP_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
 def lib():
     """Load libfastpfp.so (raises if it was not built: no fallback)."""
     global _lib
     if _lib is not None:
         return _lib
+    _nccl_hint()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1207_1114_b200.build` "
                           "(there is no CPU fallback)")
@@ -70,6 +86,8 @@ def lib():
     H, I64, I32, D, FP, VP = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p, C.c_void_p
     sig = {
         "fastpfp_create": (C.c_int, [I64, I64, I64, C.POINTER(H)]),
+        "fastpfp_create_dist": (C.c_int, [I64, I64, I64, C.c_int, C.c_int, VP, C.POINTER(H)]),
+        "fastpfp_nccl_unique_id": (C.c_int, [VP, I64]),
         "fastpfp_set_graphs": (C.c_int, [H, FP, FP, FP, FP, C.c_int]),
         "fastpfp_set_x0": (C.c_int, [H, FP, C.c_int]),
         "fastpfp_reset": (C.c_int, [H]),
@@ -143,15 +161,33 @@ class IterReport:
     mu: List[float] = field(default_factory=list)
 
 
-class Solver:
-    """One FastPFP problem instance on the current CUDA device (fastpfp_create ... destroy)."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Solver(..., dist=(rank, world, uid)) (create on rank 0)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().fastpfp_nccl_unique_id(buf, 128))
+    return buf.raw
 
-    def __init__(self, n: int, n_prime: int, d: int = 0):
+
+class Solver:
+    """One FastPFP problem instance on the current CUDA device (fastpfp_create ... destroy).
+
+    dist=(rank, world, uid) creates the row-sharded handle (fastpfp_create_dist): this rank owns
+    rows [rank*n/world, (rank+1)*n/world) of A, B and X."""
+
+    def __init__(self, n: int, n_prime: int, d: int = 0, dist=None):
         L = lib()
         h = C.c_void_p()
-        _check(L.fastpfp_create(n, n_prime, d, C.byref(h)))
+        self.rank, self.world = 0, 1
+        if dist is None:
+            _check(L.fastpfp_create(n, n_prime, d, C.byref(h)))
+        else:
+            rank, world, uid = dist
+            ub = C.create_string_buffer(bytes(uid), 128)
+            _check(L.fastpfp_create_dist(n, n_prime, d, int(rank), int(world), ub, C.byref(h)))
+            self.rank, self.world = int(rank), int(world)
         self._h = h
-        self.n, self.n_prime, self.d = n, n_prime, d
+        self.n_glob = n
+        self.n, self.n_prime, self.d = n // self.world, n_prime, d
 
     # -- lifecycle --------------------------------------------------------------------------
     def close(self):
@@ -183,7 +219,7 @@ class Solver:
         dev = da
         if any(x is not None and d != dev for x, d in ((Ap, dp), (B, db), (Bp, dbp))):
             raise ValueError("all inputs must live on the same side (host or device)")
-        self._check_shape(A, (self.n, self.n)); self._check_shape(Ap, (self.n_prime, self.n_prime))
+        self._check_shape(A, (self.n, self.n_glob)); self._check_shape(Ap, (self.n_prime, self.n_prime))
         if self.d > 0:
             self._check_shape(B, (self.n, self.d)); self._check_shape(Bp, (self.n_prime, self.d))
         _check(lib().fastpfp_set_graphs(self._h, pa, pp, pb, pbp, dev), self._h)
@@ -244,7 +280,7 @@ class Solver:
         _check(lib().fastpfp_reset_stats(self._h), self._h)
 
     def discretize(self):
-        out = np.empty(self.n, np.int32)
+        out = np.empty(self.n_glob, np.int32)
         _check(lib().fastpfp_discretize(self._h, out.ctypes.data), self._h)
         return out
 

@@ -15,6 +15,7 @@
 
 #include "../../include/fastpfp.h"
 #include "common.cuh"
+#include "nccl_dyn.h"
 
 using namespace fpfp;
 
@@ -31,7 +32,14 @@ struct Buf {
 }  // namespace
 
 struct fastpfp_handle {
-  int64_t n = 0, np = 0, d = 0, m = 0;
+  // n: rows of A/X/K held by this handle (= n_glob on one GPU, n_glob / world when row-sharded)
+  int64_t n = 0, np = 0, d = 0, m = 0, n_glob = 0, yrows = 0;
+  // row sharding (fastpfp_create_dist): rank r owns rows [r*n, (r+1)*n) of A, X, K, Y
+  int rank = 0, world = 1;
+  bool dist = false;
+  ncclComm_t comm = nullptr;
+  const NcclApi* nccl = nullptr;
+  Buf Uball, Usall;                 // gathered U blocks [world][n'][n]
   int device = 0, num_sms = 0, arch = 0;
   // graphs and their TF32 splits
   Buf A, Ab, As, Ap, Apb, Aps, B, Bp, K;
@@ -93,6 +101,13 @@ int set_err(fastpfp_handle* h, int code, const char* fmt, ...) {
                                            cudaGetErrorString(e0_));        \
   } while (0)
 
+#define NK(h, call)                                                                            \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      return set_err((h), FASTPFP_ENCCL, "%s failed: %s", #call, (h)->nccl->GetErrorString(r_)); \
+  } while (0)
+
 cudaError_t alloc_buf(Buf& b, int rows, int cols) {
   b.rows = rows;
   b.cols = cols;
@@ -130,15 +145,15 @@ cudaError_t download(const Buf& b, float* dst, int is_device, cudaStream_t s) {
 
 // projection tiling: largest TR in {128, 64, 32, 16, 8} giving >= 2 tiles per SM, else 8
 void plan_projection(fastpfp_handle* h) {
-  const int64_t m = h->m;
+  const int64_t m = h->m, rows = h->yrows;
   const int CB = (int)ceil_div(m, kProjTC);
   int TR = 8;
   for (int tr : {128, 64, 32, 16, 8}) {
-    if (ceil_div(m, tr) * CB >= 2LL * h->num_sms) { TR = tr; break; }
+    if (ceil_div(rows, tr) * CB >= 2LL * h->num_sms) { TR = tr; break; }
   }
   h->TR = TR;
   h->CB = CB;
-  h->RB = (int)ceil_div(m, TR);
+  h->RB = (int)ceil_div(rows, TR);
   h->RBx = (int)ceil_div(h->n, TR);
   h->CBx = (int)ceil_div(h->np, kProjTC);
   const int64_t want = std::max<int64_t>((int64_t)h->RB * h->CB, (int64_t)h->RBx * h->CBx);
@@ -171,10 +186,10 @@ int reset_state(fastpfp_handle* h) {
                             cudaMemcpyDeviceToDevice, s));
   } else {
     CK(h, launch_fill(h->X.p, h->X.ld, (int)h->n, (int)h->np,
-                      (float)(1.0 / ((double)h->n * (double)h->np)), s));  // 11^T/(nn')
+                      (float)(1.0 / ((double)h->n_glob * (double)h->np)), s));  // 11^T/(nn')
   }
   CK(h, launch_split(h->X.p, h->X.ld, h->Xb.p, h->Xs.p, h->X.ld, (int)h->n, (int)h->np, s));
-  CK(h, cudaMemsetAsync(h->Y.p, 0, (size_t)h->m * h->Y.ld * sizeof(float), s));  // Y = 0
+  CK(h, cudaMemsetAsync(h->Y.p, 0, (size_t)h->yrows * h->Y.ld * sizeof(float), s));  // Y = 0
   CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
   CK(h, cudaStreamSynchronize(s));
   h->t = 0;
@@ -231,8 +246,9 @@ void fastpfp_destroy(fastpfp_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (Buf* b : {&h->A, &h->Ab, &h->As, &h->Ap, &h->Apb, &h->Aps, &h->B, &h->Bp, &h->K, &h->X,
-                 &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G})
+                 &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G, &h->Uball, &h->Usall})
     free_buf(*b);
+  if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
                   (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal})
@@ -244,9 +260,10 @@ void fastpfp_destroy(fastpfp_handle* h) {
   delete h;
 }
 
-int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) {
-  if (!out || n < 1 || n_prime < 1 || d < 0 || n > (1 << 20) || n_prime > (1 << 20) ||
-      d > (1 << 20))
+static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int world,
+                       const void* nccl_id, fastpfp_handle** out) {
+  if (!out || n_glob < 1 || n_prime < 1 || d < 0 || n_glob > (1 << 20) || n_prime > (1 << 20) ||
+      d > (1 << 20) || world < 1 || rank < 0 || rank >= world)
     return FASTPFP_EINVAL;
   *out = nullptr;
   int dev = 0;
@@ -254,8 +271,14 @@ int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) 
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   if (major != 10) return FASTPFP_ENODEV;
+  const bool dist = nccl_id != nullptr;
+  if (dist && (n_glob < n_prime || n_glob % world != 0 || (n_glob / world) % 32 != 0))
+    return FASTPFP_EUNSUPPORTED;   // row sharding needs n >= n' and n/P a multiple of 32
   fastpfp_handle* h = new fastpfp_handle();
-  h->n = n; h->np = n_prime; h->d = d; h->m = std::max(n, n_prime);
+  h->n_glob = n_glob; h->n = n_glob / world; h->np = n_prime; h->d = d;
+  h->m = std::max(n_glob, n_prime);
+  h->yrows = dist ? h->n : h->m;
+  h->rank = rank; h->world = world; h->dist = dist;
   h->device = dev;
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
   h->arch = fastpfp_device_arch();
@@ -264,25 +287,39 @@ int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) 
     if (e != cudaSuccess && rc == FASTPFP_OK)
       rc = (e == cudaErrorMemoryAllocation) ? FASTPFP_ENOMEM : FASTPFP_ECUDA;
   };
-  const int N = (int)n, NP = (int)n_prime, M = (int)h->m, D = (int)d;
-  A(alloc_buf(h->A, N, N)); A(alloc_buf(h->Ab, N, N)); A(alloc_buf(h->As, N, N));
+  const int N = (int)h->n, NG = (int)n_glob, NP = (int)n_prime, M = (int)h->m, D = (int)d;
+  A(alloc_buf(h->A, N, NG)); A(alloc_buf(h->Ab, N, NG)); A(alloc_buf(h->As, N, NG));
   A(alloc_buf(h->Ap, NP, NP)); A(alloc_buf(h->Apb, NP, NP)); A(alloc_buf(h->Aps, NP, NP));
   if (D > 0) { A(alloc_buf(h->B, N, D)); A(alloc_buf(h->Bp, NP, D)); }
   A(alloc_buf(h->K, N, NP));
   A(alloc_buf(h->X, N, NP)); A(alloc_buf(h->Xb, N, NP)); A(alloc_buf(h->Xs, N, NP));
-  A(alloc_buf(h->U, NP, N)); A(alloc_buf(h->Ub, NP, N)); A(alloc_buf(h->Us, NP, N));
-  A(alloc_buf(h->Y, M, M));
+  A(alloc_buf(h->Ub, NP, N)); A(alloc_buf(h->Us, NP, N));
+  if (!dist) A(alloc_buf(h->U, NP, N));     // plain U: SIMT GEMM2 only
+  if (dist) { A(alloc_buf(h->Uball, world * NP, N)); A(alloc_buf(h->Usall, world * NP, N)); }
+  A(alloc_buf(h->Y, (int)h->yrows, M));
   plan_projection(h);
-  A(alloc_arr(h->rowpart, (size_t)h->CB * M));
+  A(alloc_arr(h->rowpart, (size_t)h->CB * h->yrows));
   A(alloc_arr(h->colpart, (size_t)h->RB * M));
-  A(alloc_arr(h->r, M)); A(alloc_arr(h->c, M));
+  A(alloc_arr(h->r, h->yrows)); A(alloc_arr(h->c, (size_t)M + 1));
   A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
-  A(alloc_arr(h->scal, 4));
+  A(alloc_arr(h->scal, 8));
   A(cudaMallocHost(&h->h_iters, kMaxCheck * sizeof(DevIter)));
   A(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
+  if (rc == FASTPFP_OK && dist) {
+    std::string msg;
+    h->nccl = nccl_api(msg);
+    if (!h->nccl) {
+      h->err = msg;
+      rc = FASTPFP_ENCCL;
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      if (h->nccl->CommInitRank(&h->comm, world, id, rank) != ncclSuccess) rc = FASTPFP_ENCCL;
+    }
+  }
   if (rc != FASTPFP_OK) {
     cudaGetLastError();
     fastpfp_destroy(h);
@@ -290,6 +327,27 @@ int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) 
   }
   *out = h;
   return FASTPFP_OK;
+}
+
+int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out) {
+  return create_impl(n, n_prime, d, 0, 1, nullptr, out);
+}
+
+int fastpfp_nccl_unique_id(void* out, int64_t size) {
+  if (!out || size < (int64_t)sizeof(ncclUniqueId)) return FASTPFP_EINVAL;
+  std::string msg;
+  const NcclApi* api = nccl_api(msg);
+  if (!api) return FASTPFP_ENCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return FASTPFP_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return FASTPFP_OK;
+}
+
+int fastpfp_create_dist(int64_t n, int64_t n_prime, int64_t d, int rank, int world,
+                        const void* nccl_id, fastpfp_handle** out) {
+  if (!nccl_id) return FASTPFP_EINVAL;
+  return create_impl(n, n_prime, d, rank, world, nccl_id, out);
 }
 
 int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
@@ -341,13 +399,17 @@ int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, 
   CK(h, upload(h->A, A, is_device, s));
   CK(h, upload(h->Ap, A_prime, is_device, s));
   CK(h, cudaMemsetAsync(h->flags, 0, sizeof(int), s));
-  CK(h, launch_check_sym(h->A.p, h->A.ld, (int)h->n, h->flags, s));
+  if (h->dist) {   // local row block: finiteness here, symmetry is the caller's contract
+    CK(h, launch_check_finite(h->A.p, h->A.ld, (int)h->n, (int)h->n_glob, h->flags, s));
+  } else {
+    CK(h, launch_check_sym(h->A.p, h->A.ld, (int)h->n, h->flags, s));
+  }
   int rc = check_flags(h, "A");
   if (rc) return rc;
   CK(h, launch_check_sym(h->Ap.p, h->Ap.ld, (int)h->np, h->flags, s));
   rc = check_flags(h, "A'");
   if (rc) return rc;
-  CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n, s));
+  CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n_glob, s));
   CK(h, launch_split(h->Ap.p, h->Ap.ld, h->Apb.p, h->Aps.p, h->Ap.ld, (int)h->np, (int)h->np, s));
   if (h->d > 0) {
     CK(h, upload(h->B, B, is_device, s));
@@ -393,9 +455,158 @@ int fastpfp_reset(fastpfp_handle* h) {
   return reset_state(h);
 }
 
+// ---- row-sharded outer iteration: every step is a local kernel; the three
+// exchanges are NCCL collectives on the handle's stream: all-gather of U's TF32 parts after GEMM1,
+// all-reduce SUM of [column sums | sigma] after every sweep, all-reduce MAX of mu and of rho.
+static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo, bool add_k) {
+  cudaStream_t s = h->stream;
+  const int N = (int)h->n, NP = (int)h->np;
+  // U_r = A' X_r^T for the local rows r
+  GemmArgs g1{};
+  g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
+  g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
+  g1.M = NP; g1.N = N; g1.K = NP;
+  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->Ub.ld;
+  int rc = run_gemm(h, g1);
+  if (rc) return rc;
+  const size_t cnt = (size_t)NP * h->Ub.ld;
+  NK(h, h->nccl->GroupStart());
+  NK(h, h->nccl->AllGather(h->Ub.p, h->Uball.p, cnt, ncclFloat32, h->comm, s));
+  NK(h, h->nccl->AllGather(h->Us.p, h->Usall.p, cnt, ncclFloat32, h->comm, s));
+  NK(h, h->nccl->GroupEnd());
+  // Y_r[:, 0:n'] = A_r U^T + lambda K_r, K-loop over the gathered rank blocks
+  GemmArgs g2{};
+  g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
+  g2.Qb = h->Uball.p; g2.Qs = h->Usall.p; g2.ldQ = h->Uball.ld;
+  g2.M = N; g2.N = NP; g2.K = (int)h->n_glob;
+  g2.q_blocks = h->world; g2.q_block_k = N; g2.q_block_stride = (int64_t)NP * h->Uball.ld;
+  g2.epi = kEpiAxpy; g2.C = out; g2.ldC = ldo;
+  g2.D = (add_k && lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
+  g2.lam = (float)lambda;
+  return run_gemm(h, g2);
+}
+
+static ProjArgs dist_proj_args(fastpfp_handle* h, int mode, double alpha, double eps1, double eps2) {
+  ProjArgs pa{};
+  pa.mode = mode; pa.rows = (int)h->yrows;
+  pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
+  pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = (int)h->n;
+  pa.np = (int)h->np;
+  pa.alpha = alpha; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = 1;
+  pa.rescale = h->rescale; pa.split = 1;
+  pa.TR = h->TR; pa.RB = h->RB; pa.CB = h->CB; pa.RBx = h->RBx; pa.CBx = h->CBx;
+  pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c; pa.scal = h->scal;
+  pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;
+  pa.rho_part = h->rho_part; pa.iter_out = h->iters; pa.done = h->done;
+  return pa;
+}
+
+static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps1, double eps2,
+                      int32_t max_iter2, DevIter& out) {
+  cudaStream_t s = h->stream;
+  if (h->profile) CK(h, cudaEventRecord(h->ev[0], s));
+  int rc = dist_gemms(h, lambda, h->Y.p, h->Y.ld, true);
+  if (rc) return rc;
+  if (h->profile) CK(h, cudaEventRecord(h->ev[1], s));
+  if (h->slack_mode == 1 && h->m > h->np) {
+    CK(h, launch_zero_slack(h->Y.p, h->Y.ld, (int)h->yrows, (int)h->m, (int)h->n, (int)h->np,
+                            h->done, s));
+    h->stats.launches += 1;
+  }
+  const size_t mc = (size_t)h->m + 1;
+  ProjArgs pa = dist_proj_args(h, kProjSums, alpha, eps1, eps2);
+  CK(h, launch_proj(pa, h->grid, s));
+  NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
+  h->stats.launches += 1;
+  int sweeps = 0;
+  double delta = 0.0;
+  for (;;) {
+    pa.mode = kProjOneSweep;
+    CK(h, launch_proj(pa, h->grid, s));
+    NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
+    NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
+    h->stats.launches += 1;
+    ++sweeps;
+    if (sweeps >= max_iter2) break;
+    if (eps2 > 0.0) {   // the inner stop needs the global delta on the host
+      CK(h, cudaMemcpyAsync(&delta, h->scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(h, cudaStreamSynchronize(s));
+      if (delta < eps2) break;
+    }
+  }
+  pa.mode = kProjFinMu;
+  CK(h, launch_proj(pa, h->grid, s));
+  NK(h, h->nccl->AllReduce(h->scal + 1, h->scal + 1, 1, ncclFloat64, ncclMax, h->comm, s));
+  pa.mode = kProjFinApply;
+  CK(h, launch_proj(pa, h->grid, s));
+  NK(h, h->nccl->AllReduce(h->scal + 2, h->scal + 2, 1, ncclFloat64, ncclMax, h->comm, s));
+  h->stats.launches += 2;
+  h->stats.proj_launches += 1;
+  if (h->profile) CK(h, cudaEventRecord(h->ev[2], s));
+  double sc[3];
+  CK(h, cudaMemcpyAsync(sc, h->scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(h, cudaStreamSynchronize(s));
+  out = DevIter{};
+  out.valid = 1; out.sweeps = sweeps; out.delta = sc[0]; out.mu = sc[1];
+  if (sc[2] < 0.0) {
+    out.degenerate = 1;
+  } else {
+    out.rho = sc[2];
+    out.converged = sc[2] < eps1;
+  }
+  if (h->profile) {
+    float g_ms = 0.f, p_ms = 0.f;
+    CK(h, cudaEventElapsedTime(&g_ms, h->ev[0], h->ev[1]));
+    CK(h, cudaEventElapsedTime(&p_ms, h->ev[1], h->ev[2]));
+    h->stats.gemm_ms += g_ms;
+    h->stats.proj_ms += p_ms;
+    h->stats.gemm_flops += 2.0 * (double)h->n * h->np * ((double)h->n_glob + h->np);
+  }
+  return FASTPFP_OK;
+}
+
 int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1, double eps2,
                     int32_t max_iter1, int32_t max_iter2, float* X_out, fastpfp_report* rep) {
   GUARD(h);
+  if (h->dist && h->graphs_set && (alpha >= 0.0 && alpha <= 1.0) && lambda >= 0.0 &&
+      std::isfinite(lambda) && eps1 >= 0.0 && eps2 >= 0.0 && max_iter1 >= 1 && max_iter2 >= 1) {
+    if (h->precision == 2) return set_err(h, FASTPFP_EUNSUPPORTED, "row sharding needs the tensor-core GEMM");
+    fastpfp_report R{};
+    if (rep) {
+      R.trace_capacity = rep->trace_capacity;
+      R.rho_trace = rep->rho_trace; R.sweeps_trace = rep->sweeps_trace;
+      R.delta_trace = rep->delta_trace; R.mu_trace = rep->mu_trace;
+    }
+    CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    for (int32_t k = 0; k < max_iter1; ++k) {
+      DevIter it{};
+      int rc = dist_outer(h, alpha, lambda, eps1, eps2, max_iter2, it);
+      if (rc) return rc;
+      h->stats.outer_iterations += 1;
+      h->stats.sweeps += it.sweeps;
+      R.total_sweeps += it.sweeps;
+      R.last_delta = it.delta;
+      R.last_mu = it.mu;
+      if (it.degenerate) { R.degenerate = 1; break; }
+      if (R.trace_capacity > R.iterations) {
+        const int q = R.iterations;
+        if (R.rho_trace) R.rho_trace[q] = it.rho;
+        if (R.sweeps_trace) R.sweeps_trace[q] = it.sweeps;
+        if (R.delta_trace) R.delta_trace[q] = it.delta;
+        if (R.mu_trace) R.mu_trace[q] = it.mu;
+      }
+      R.iterations += 1;
+      R.last_rho = it.rho;
+      h->t += 1;
+      if (it.converged) { R.converged = 1; break; }
+    }
+    if (X_out) {
+      CK(h, download(h->X, X_out, 0, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
+    }
+    if (rep) *rep = R;
+    return FASTPFP_OK;
+  }
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   if (!(alpha >= 0.0 && alpha <= 1.0) || !(lambda >= 0.0) || !std::isfinite(lambda) ||
       !(eps1 >= 0.0) || !(eps2 >= 0.0) || max_iter1 < 1 || max_iter2 < 1)
@@ -439,11 +650,12 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       if (rc) return rc;
       if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 1], s));
       if (h->slack_mode == 1 && h->m > std::min(h->n, h->np)) {
-        CK(h, launch_zero_slack(h->Y.p, h->Y.ld, (int)h->m, N, NP, h->done, s));
+        CK(h, launch_zero_slack(h->Y.p, h->Y.ld, (int)h->m, (int)h->m, N, NP, h->done, s));
         h->stats.launches += 1;
       }
       // lines 4-9: projection loop, blend, rescale (one persistent kernel)
       ProjArgs pa{};
+      pa.mode = kProjFull; pa.rows = (int)h->yrows;
       pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
       pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = N; pa.np = NP;
       pa.alpha = alpha; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = max_iter2;
@@ -533,6 +745,18 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   if (!h->G.p) CK(h, alloc_buf(h->G, (int)h->n, (int)h->np));
   cudaStream_t s = h->stream;
+  if (h->dist) {
+    int rc = dist_gemms(h, lambda, h->G.p, h->G.ld, false);
+    if (rc) return rc;
+    CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, (int)h->n, (int)h->np,
+                      h->scal + 4, s));
+    NK(h, h->nccl->AllReduce(h->scal + 4, h->scal + 4, 2, ncclFloat64, ncclSum, h->comm, s));
+    double v[2];
+    CK(h, cudaMemcpyAsync(v, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(h, cudaStreamSynchronize(s));
+    *f = 0.5 * v[0] + lambda * v[1];
+    return FASTPFP_OK;
+  }
   const int N = (int)h->n, NP = (int)h->np;
   GemmArgs g1{};
   g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
@@ -562,6 +786,17 @@ int fastpfp_discretize(fastpfp_handle* h, int32_t* assign) {
   if (!assign) return FASTPFP_EINVAL;
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   std::string msg;
+  if (h->dist) {   // gather the full X (every rank gets the same greedy result)
+    Buf Xall;
+    CK(h, alloc_buf(Xall, (int)h->n_glob, (int)h->np));
+    const size_t cnt = (size_t)h->n * h->X.ld;
+    ncclResult_t nr = h->nccl->AllGather(h->X.p, Xall.p, cnt, ncclFloat32, h->comm, h->stream);
+    if (nr != ncclSuccess) { free_buf(Xall); return set_err(h, FASTPFP_ENCCL, "all-gather X"); }
+    int rc = fpfp_discretize_device(h, Xall.p, Xall.ld, (int)h->n_glob, (int)h->np, assign, h->stream, msg);
+    free_buf(Xall);
+    if (rc) return set_err(h, rc, "%s", msg.c_str());
+    return FASTPFP_OK;
+  }
   int rc = fpfp_discretize_device(h, h->X.p, h->X.ld, (int)h->n, (int)h->np, assign, h->stream, msg);
   if (rc) return set_err(h, rc, "%s", msg.c_str());
   return FASTPFP_OK;
@@ -574,7 +809,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FASTPFP_ENODEV;
   fastpfp_handle tmp;
-  tmp.n = m; tmp.np = m; tmp.m = m; tmp.device = dev;
+  tmp.n = m; tmp.np = m; tmp.m = m; tmp.n_glob = m; tmp.yrows = m; tmp.device = dev;
   cudaDeviceGetAttribute(&tmp.num_sms, cudaDevAttrMultiProcessorCount, dev);
   plan_projection(&tmp);
   Buf Yp;
@@ -583,13 +818,14 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
   auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
   A(alloc_buf(Yp, (int)m, (int)m));
   A(alloc_arr(tmp.rowpart, (size_t)tmp.CB * m)); A(alloc_arr(tmp.colpart, (size_t)tmp.RB * m));
-  A(alloc_arr(tmp.r, m)); A(alloc_arr(tmp.c, m));
+  A(alloc_arr(tmp.r, m)); A(alloc_arr(tmp.c, m + 1));
   A(alloc_arr(tmp.sig_part, tmp.grid)); A(alloc_arr(tmp.mu_part, tmp.grid));
   A(alloc_arr(tmp.dlt_part, tmp.grid)); A(alloc_arr(tmp.rho_part, tmp.grid));
   A(alloc_arr(tmp.iters, 1)); A(alloc_arr(tmp.done, 1));
   if (rc == FASTPFP_OK) {
     A(upload(Yp, Y, 1, s));
     ProjArgs pa{};
+    pa.mode = kProjFull; pa.rows = (int)m;
     pa.Y = Yp.p; pa.ldY = Yp.ld; pa.m = (int)m; pa.n = (int)m; pa.np = (int)m;
     pa.eps2 = eps2; pa.max_iter2 = max_iter2; pa.do_finalize = 0; pa.do_sums = 1;
     pa.TR = tmp.TR; pa.RB = tmp.RB; pa.CB = tmp.CB; pa.RBx = tmp.RBx; pa.CBx = tmp.CBx;

@@ -45,8 +45,12 @@ struct DevIter {
 };
 
 // Arguments of the persistent projection + finalize kernel (proj.cu).
+enum ProjMode { kProjFull = 0, kProjSums = 1, kProjOneSweep = 2, kProjFinMu = 3, kProjFinApply = 4 };
+
 struct ProjArgs {
-  float* Y; int64_t ldY; int m;                // slacked matrix, m x m (row stride ldY, 16B rows)
+  int mode;                                    // ProjMode (kProjFull: whole inner loop + finalize)
+  float* Y; int64_t ldY; int m;                // slacked matrix, rows x m (row stride ldY, 16B rows)
+  int rows;                                    // rows of Y held here (m on one GPU, n/P when sharded)
   float* X; float* Xb; float* Xs; int64_t ldX; // soft assignment n x n' and its TF32 split
   int n, np;
   double alpha, eps1, eps2;
@@ -54,9 +58,11 @@ struct ProjArgs {
   int rescale, split, do_finalize, do_sums;
   int TR, RB, CB;        // sweep tiles: TR rows x 512 cols over m x m
   int RBx, CBx;          // finalize tiles over n x n'
-  double* rowpart;       // [CB][m]
+  double* rowpart;       // [CB][rows]
   double* colpart;       // [RB][m]
-  double* r; double* c;  // [m]
+  double* r;             // [rows]
+  double* c;             // [m + 1]: column sums, c[m] = sigma (dist all-reduce buffer)
+  double* scal;          // dist scalars: [0] delta_local, [1] mu, [2] rho (or -1: degenerate)
   double* sig_part;      // [grid]
   float* dlt_part;       // [grid]
   double* mu_part;       // [grid]
@@ -77,8 +83,8 @@ cudaError_t launch_check_sym(const float* A, int64_t lda, int n, int* flags, cud
 cudaError_t launch_check_finite(const float* A, int64_t lda, int rows, int cols, int* flags,
                                 cudaStream_t s);
 cudaError_t launch_fill(float* A, int64_t lda, int rows, int cols, float v, cudaStream_t s);
-cudaError_t launch_zero_slack(float* Y, int64_t ldY, int m, int n, int np, const int* done,
-                              cudaStream_t s);
+cudaError_t launch_zero_slack(float* Y, int64_t ldY, int rows, int m, int n, int np,
+                              const int* done, cudaStream_t s);
 cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t ld, int rows,
                         int cols, double* out2, cudaStream_t s);
 
@@ -97,6 +103,9 @@ struct GemmArgs {
   const float* D; int64_t ldD; float lam;  // kEpiAxpy: C = acc + lam * D
   const int* done;                 // nullable early-exit flag
   int cta_group = 2;               // tensor-core path: 1 = 128x128 tiles per CTA, 2 = 256x256 per CTA pair
+  // row-sharded GEMM2: Q = [q_blocks][N][q_block_k] (one block per rank, block stride in floats)
+  int q_blocks = 1, q_block_k = 0;
+  int64_t q_block_stride = 0;
 };
 // Batched small-pair whole solve (small_solve.cu), n, n' <= 128, one pair per CTA.
 struct SmallArgs {

@@ -111,6 +111,23 @@ __device__ __forceinline__ void tma_load(const CUtensorMap* map, uint32_t dst, u
   }
 }
 
+// 3-D variant: Q gathered from P ranks as [block][rows][qk] (row-sharded pair)
+template <int CG>
+__device__ __forceinline__ void tma_load3(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0,
+                                          int c1, int c2) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
+}
+
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row core groups 1024 B apart).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   uint64_t d = 0;
@@ -178,6 +195,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 struct TcParams {
   int M, N, K;
+  int q3d, qk;      // Q is [K/qk][N][qk] blocks (3-D tensor map) when q3d != 0
   int epi;
   float* C; float* C2; float* C3; int64_t ldC;
   const float* D; int64_t ldD; float lam;
@@ -266,10 +284,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
           const int kc = kb * kBK;
           tma_load<CG>(&mPb, base + 0 * kBoxBytes, bar, kc, prow);
-          tma_load<CG>(&mQb, base + 1 * kBoxBytes, bar, kc, qrow);
+          if (p.q3d) {
+            const int blk = kc / p.qk, kin = kc - blk * p.qk;
+            tma_load3<CG>(&mQb, base + 1 * kBoxBytes, bar, kin, qrow, blk);
+          } else {
+            tma_load<CG>(&mQb, base + 1 * kBoxBytes, bar, kc, qrow);
+          }
           if (PASSES == 3) {
             tma_load<CG>(&mPs, base + 2 * kBoxBytes, bar, kc, prow);
-            tma_load<CG>(&mQs, base + 3 * kBoxBytes, bar, kc, qrow);
+            if (p.q3d) {
+              const int blk = kc / p.qk, kin = kc - blk * p.qk;
+              tma_load3<CG>(&mQs, base + 3 * kBoxBytes, bar, kin, qrow, blk);
+            } else {
+              tma_load<CG>(&mQs, base + 3 * kBoxBytes, bar, kc, qrow);
+            }
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -444,15 +472,34 @@ bool make_map(CUtensorMap* m, const float* base, int rows, int K, int64_t ld) {
   return r == CUDA_SUCCESS;
 }
 
+// [blocks][rows][qk] blocks of row stride ld and block stride bstride (floats); box 128 x 32 x 1
+bool make_map3(CUtensorMap* m, const float* base, int rows, int qk, int blocks, int64_t ld,
+               int64_t bstride) {
+  cuuint64_t dims[3] = {(cuuint64_t)qk, (cuuint64_t)rows, (cuuint64_t)blocks};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * sizeof(float)), (cuuint64_t)(bstride * sizeof(float))};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)kRowsPerCta, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int CG, int PASSES>
 cudaError_t launch_impl(const GemmArgs& g, cudaStream_t s, int device) {
   CUtensorMap mPb, mPs, mQb, mQs;
   const float* ps = PASSES == 3 ? g.Ps : g.Pb;
   const float* qs = PASSES == 3 ? g.Qs : g.Qb;
-  if (!make_map(&mPb, g.Pb, g.M, g.K, g.ldP) || !make_map(&mPs, ps, g.M, g.K, g.ldP) ||
-      !make_map(&mQb, g.Qb, g.N, g.K, g.ldQ) || !make_map(&mQs, qs, g.N, g.K, g.ldQ))
-    return cudaErrorInvalidValue;
-  TcParams p{g.M, g.N, g.K, g.epi, g.C, g.C2, g.C3, g.ldC, g.D, g.ldD, g.lam, g.done};
+  const bool q3d = g.q_blocks > 1;
+  bool ok = make_map(&mPb, g.Pb, g.M, g.K, g.ldP) && make_map(&mPs, ps, g.M, g.K, g.ldP);
+  if (q3d)
+    ok = ok && make_map3(&mQb, g.Qb, g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride) &&
+         make_map3(&mQs, qs, g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride);
+  else
+    ok = ok && make_map(&mQb, g.Qb, g.N, g.K, g.ldQ) && make_map(&mQs, qs, g.N, g.K, g.ldQ);
+  if (!ok) return cudaErrorInvalidValue;
+  TcParams p{g.M, g.N, g.K, q3d ? 1 : 0, q3d ? g.q_block_k : 0, g.epi, g.C, g.C2, g.C3, g.ldC,
+             g.D, g.ldD, g.lam, g.done};
   constexpr int kBoxes = PASSES == 1 ? 2 : 4;
   const size_t smem = (size_t)kStages * kBoxes * kBoxBytes + 1024;
   auto kern = gemm_tc_kernel<CG, PASSES>;
@@ -488,6 +535,8 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (!g.Pb || !g.Qb || g.M < 1 || g.N < 1 || g.K < 1) return false;
   // TMA: 16-byte aligned bases and row strides
   auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % 16) == 0; };
+  if (g.q_blocks > 1 && (g.q_block_k % kBK != 0 || (int64_t)g.q_block_k * g.q_blocks != g.K))
+    return false;
   return al(g.Pb) && al(g.Ps) && al(g.Qb) && al(g.Qs) && (g.ldP % 4 == 0) && (g.ldQ % 4 == 0) &&
          (g.ldC % 4 == 0);
 }

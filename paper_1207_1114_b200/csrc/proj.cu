@@ -44,7 +44,7 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = rb * p.TR;
-  const int row1 = min(p.m, row0 + p.TR);
+  const int row1 = min(p.rows, row0 + p.TR);
   const int colbase = cb * kProjTC;
   const double inv_m = 1.0 / (double)p.m;
 
@@ -98,7 +98,7 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
         if (inrow[q]) *reinterpret_cast<float4*>(rowp + q * 128) = v[q];
     }
     racc = warp_sum(racc);
-    if (lane == 0) p.rowpart[(int64_t)cb * p.m + i] = racc;
+    if (lane == 0) p.rowpart[(int64_t)cb * p.rows + i] = racc;
   }
   // column partials of this tile: combine the 8 warps in a fixed order
 #pragma unroll
@@ -132,10 +132,10 @@ __device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
     s = warp_sum(s);
     if (lane == 0) { p.c[j] = s; local += s; }
   }
-  for (int i = gw; i < p.m; i += nw) {
+  for (int i = gw; i < p.rows; i += nw) {
     double s = 0.0;
 #pragma unroll 4
-    for (int cb = lane; cb < p.CB; cb += 32) s += p.rowpart[(int64_t)cb * p.m + i];
+    for (int cb = lane; cb < p.CB; cb += 32) s += p.rowpart[(int64_t)cb * p.rows + i];
     s = warp_sum(s);
     if (lane == 0) p.r[i] = s;
   }
@@ -194,48 +194,16 @@ __device__ __forceinline__ T grid_max(const T* parts, ProjSmem& sm, T init) {
   return r;
 }
 
-__global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
-  if (*p.done) return;  // an earlier iteration of this launch batch converged (uniform)
-  cg::grid_group grid = cg::this_grid();
-  __shared__ ProjSmem sm;
-  const int ntiles = p.RB * p.CB;
-  float dummy = 0.0f;
-
-  if (p.do_sums) {
-    // sums of the current Y (fresh GEMM block + retained slack)
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
-    grid.sync();
-    reduce_phase(p, sm);
-    grid.sync();
+// Block 0 folds the per-block sigma partials (fixed order) into c[m] (the dist all-reduce buffer).
+__device__ __forceinline__ void publish_sigma(const ProjArgs& p, ProjSmem& sm) {
+  if (blockIdx.x == 0) {
+    const double sg = grid_sigma(p, sm);
+    if (threadIdx.x == 0) p.c[p.m] = sg;
   }
-  double sigma = grid_sigma(p, sm);
+}
 
-  int sweeps = 0;
-  float delta = 0.0f;
-  for (;;) {
-    float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
-    dmax = block_max(dmax, sm, 0.0f);
-    if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
-    grid.sync();
-    reduce_phase(p, sm);
-    grid.sync();
-    sigma = grid_sigma(p, sm);
-    delta = grid_max(p.dlt_part, sm, 0.0f);
-    ++sweeps;
-    if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
-  }
-
-  if (!p.do_finalize) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      p.iter_out->valid = 1;
-      p.iter_out->sweeps = sweeps;
-      p.iter_out->delta = (double)delta;
-    }
-    return;
-  }
-
-  // ---- Algorithm 1 line 8: X~ = (1 - alpha) X + alpha Y[0:n, 0:n'];  line 9: X = X~ / max X~
+// X~ = (1 - alpha) X + alpha Y[0:n, 0:n'] (Algorithm 1 line 8) and its local max (line 9's mu).
+__device__ __forceinline__ double finalize_mu(const ProjArgs& p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ftiles = p.RBx * p.CBx;
   const double a = p.alpha, b = 1.0 - p.alpha;
@@ -258,18 +226,14 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
       }
     }
   }
-  mu_loc = block_max(mu_loc, sm, (double)-INFINITY);
-  if (threadIdx.x == 0) p.mu_part[blockIdx.x] = mu_loc;
-  grid.sync();
-  const double mu = grid_max(p.mu_part, sm, (double)-INFINITY);
-  if (!(mu > 1e-300)) {  // degenerate guard (reading A7): X left unchanged, loop stops
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->degenerate = 1;
-      p.iter_out->delta = (double)delta; p.iter_out->mu = mu; p.iter_out->rho = 0.0;
-      *p.done = 1;
-    }
-    return;
-  }
+  return mu_loc;
+}
+
+// X = X~ / mu (if rescale), TF32 split of X, local max |X_new - X_old|.
+__device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ftiles = p.RBx * p.CBx;
+  const double a = p.alpha, b = 1.0 - p.alpha;
   const double inv_scale = p.rescale ? mu : 1.0;
   float rho_loc = 0.0f;
   for (int t = blockIdx.x; t < ftiles; t += gridDim.x) {
@@ -308,7 +272,116 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
       }
     }
   }
-  rho_loc = block_max(rho_loc, sm, 0.0f);
+  return rho_loc;
+}
+
+__global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
+  if (*p.done) return;  // an earlier iteration of this launch batch converged (uniform)
+  cg::grid_group grid = cg::this_grid();
+  __shared__ ProjSmem sm;
+  const int ntiles = p.RB * p.CB;
+  float dummy = 0.0f;
+
+  // ------------------------------------------------------------------ distributed phases
+  if (p.mode == kProjSums) {            // sums of the local rows of Y -> c_local, r, sigma_local
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+    publish_sigma(p, sm);
+    return;
+  }
+  if (p.mode == kProjOneSweep) {        // one P1+P2 sweep with the global c, sigma = c[m]
+    const double sigma = p.c[p.m];
+    float dmax = 0.0f;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
+    dmax = block_max(dmax, sm, 0.0f);
+    if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+    publish_sigma(p, sm);
+    if (blockIdx.x == 0) {
+      const float d = grid_max(p.dlt_part, sm, 0.0f);
+      if (threadIdx.x == 0) p.scal[0] = (double)d;
+    }
+    return;
+  }
+  if (p.mode == kProjFinMu) {           // local max of X~
+    double mu_loc = block_max(finalize_mu(p), sm, (double)-INFINITY);
+    if (threadIdx.x == 0) p.mu_part[blockIdx.x] = mu_loc;
+    grid.sync();
+    if (blockIdx.x == 0) {
+      const double mu = grid_max(p.mu_part, sm, (double)-INFINITY);
+      if (threadIdx.x == 0) p.scal[1] = mu;
+    }
+    return;
+  }
+  if (p.mode == kProjFinApply) {        // apply with the global mu = scal[1]
+    const double mu = p.scal[1];
+    if (!(mu > 1e-300)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.scal[2] = -1.0;   // degenerate marker
+      return;
+    }
+    float rho_loc = block_max(finalize_apply(p, mu), sm, 0.0f);
+    if (threadIdx.x == 0) p.rho_part[blockIdx.x] = rho_loc;
+    grid.sync();
+    if (blockIdx.x == 0) {
+      const float rho = grid_max(p.rho_part, sm, 0.0f);
+      if (threadIdx.x == 0) p.scal[2] = (double)rho;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ single GPU: everything
+  if (p.do_sums) {
+    // sums of the current Y (fresh GEMM block + retained slack)
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+  }
+  double sigma = grid_sigma(p, sm);
+
+  int sweeps = 0;
+  float delta = 0.0f;
+  for (;;) {
+    float dmax = 0.0f;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
+    dmax = block_max(dmax, sm, 0.0f);
+    if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
+    grid.sync();
+    reduce_phase(p, sm);
+    grid.sync();
+    sigma = grid_sigma(p, sm);
+    delta = grid_max(p.dlt_part, sm, 0.0f);
+    ++sweeps;
+    if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
+  }
+
+  if (!p.do_finalize) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.iter_out->valid = 1;
+      p.iter_out->sweeps = sweeps;
+      p.iter_out->delta = (double)delta;
+    }
+    return;
+  }
+
+  // ---- Algorithm 1 line 8: X~ = (1 - alpha) X + alpha Y[0:n, 0:n'];  line 9: X = X~ / max X~
+  double mu_loc = block_max(finalize_mu(p), sm, (double)-INFINITY);
+  if (threadIdx.x == 0) p.mu_part[blockIdx.x] = mu_loc;
+  grid.sync();
+  const double mu = grid_max(p.mu_part, sm, (double)-INFINITY);
+  if (!(mu > 1e-300)) {  // degenerate guard (reading A7): X left unchanged, loop stops
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->degenerate = 1;
+      p.iter_out->delta = (double)delta; p.iter_out->mu = mu; p.iter_out->rho = 0.0;
+      *p.done = 1;
+    }
+    return;
+  }
+  float rho_loc = block_max(finalize_apply(p, mu), sm, 0.0f);
   if (threadIdx.x == 0) p.rho_part[blockIdx.x] = rho_loc;
   grid.sync();
   if (blockIdx.x == 0) {
@@ -366,10 +439,11 @@ __global__ void fill_kernel(float* A, int64_t lda, int rows, int cols, float v) 
   }
 }
 
-// zero every entry of Y outside the X block [0:n, 0:n'] (slack_mode = reset)
-__global__ void zero_slack_kernel(float* Y, int64_t ldY, int m, int n, int np, const int* done) {
+// zero every entry of Y (rows x m) outside the X block [0:n, 0:n'] (slack_mode = reset)
+__global__ void zero_slack_kernel(float* Y, int64_t ldY, int rows, int m, int n, int np,
+                                  const int* done) {
   if (done && *done) return;
-  const int64_t total = (int64_t)m * m;
+  const int64_t total = (int64_t)rows * m;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(k / m), j = (int)(k - (k / m) * m);
@@ -440,9 +514,9 @@ cudaError_t launch_fill(float* A, int64_t lda, int rows, int cols, float v, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_zero_slack(float* Y, int64_t ldY, int m, int n, int np, const int* done,
-                              cudaStream_t s) {
-  zero_slack_kernel<<<grid_for((int64_t)m * m), 256, 0, s>>>(Y, ldY, m, n, np, done);
+cudaError_t launch_zero_slack(float* Y, int64_t ldY, int rows, int m, int n, int np,
+                              const int* done, cudaStream_t s) {
+  zero_slack_kernel<<<grid_for((int64_t)rows * m), 256, 0, s>>>(Y, ldY, rows, m, n, np, done);
   return cudaGetLastError();
 }
 

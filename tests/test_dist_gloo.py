@@ -1,0 +1,123 @@
+"""World-size-2 CPU (gloo) tests of the row-sharded path's host logic and decomposition.
+
+The sharded GPU iteration (fastpfp_create_dist) exchanges exactly three things per outer iteration:
+an all-gather of U_r = A' X_r^T, an all-reduce SUM of the column sums (+ sigma) per sweep, and
+all-reduces MAX of mu and rho. Here two gloo ranks run that same decomposition in
+fp64 numpy with real torch.distributed collectives, using the product's partition / NCCL-id
+bootstrap helpers (paper_1207_1114_b200.dist), and must reproduce the unsharded oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from oracle import fastpfp as O
+from paper_1207_1114_b200 import dist as D
+from paper_1207_1114_b200 import inputs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _allgather_cols(U_r, world):
+    parts = [torch.zeros_like(torch.from_numpy(U_r)) for _ in range(world)]
+    tdist.all_gather(parts, torch.from_numpy(U_r))
+    return np.concatenate([p.numpy() for p in parts], axis=1)
+
+
+def _allreduce(x, op):
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    tdist.all_reduce(t, op=op)
+    return t.numpy()
+
+
+def sharded_outer(sh, A_r, Ap, K_r, X_r, Y_r, lam, alpha, eps2, max_iter2, m):
+    """One outer iteration of Algorithm 1 in the sharded decomposition."""
+    npr = Ap.shape[0]
+    U_r = Ap @ X_r.T                                   # GEMM1, local
+    U = _allgather_cols(U_r, sh.world)                 # all-gather of U blocks
+    Y_r[:, :npr] = A_r @ U.T + lam * K_r               # GEMM2 (+ lambda K), local rows
+    cs = _allreduce(np.append(Y_r.sum(0), Y_r.sum()), tdist.ReduceOp.SUM)
+    c, sigma = cs[:m], cs[m]
+    r = Y_r.sum(1)
+    sweeps = 0
+    while True:
+        Z = np.maximum(Y_r + ((1.0 + sigma / m) / m - r / m)[:, None] - (c / m)[None, :], 0.0)
+        delta = _allreduce(np.array([np.max(np.abs(Z - Y_r))]), tdist.ReduceOp.MAX)[0]
+        Y_r[:] = Z
+        cs = _allreduce(np.append(Y_r.sum(0), Y_r.sum()), tdist.ReduceOp.SUM)
+        c, sigma = cs[:m], cs[m]
+        r = Y_r.sum(1)
+        sweeps += 1
+        if delta < eps2 or sweeps >= max_iter2:
+            break
+    Xt = (1 - alpha) * X_r + alpha * Y_r[:, :npr]
+    mu = _allreduce(np.array([Xt.max()]), tdist.ReduceOp.MAX)[0]
+    Xn = Xt / mu
+    rho = _allreduce(np.array([np.max(np.abs(Xn - X_r))]), tdist.ReduceOp.MAX)[0]
+    return Xn, rho, sweeps
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # NCCL-id bootstrap helper (any backend): rank 0's bytes reach every rank
+        uid = bytes(range(128)) if rank == 0 else None
+        got = D.broadcast_uid(uid, rank, world)
+        assert got == bytes(range(128))
+        for (n, npr, d) in [(64, 64, 3), (64, 50, 2)]:
+            p = inputs.planted_unequal(11 + npr, n, npr, d=d) if n != npr else \
+                inputs.config5(n=n, d=d)
+            sh = D.row_partition(n, npr, world, rank)
+            A_r, Ap, B_r, Bp = D.local_inputs(p, sh)
+            K_r = O.affinity(B_r, Bp, sh.rows, npr)
+            m = max(n, npr)
+            X_r = np.full((sh.rows, npr), 1.0 / (n * npr))
+            Y_r = np.zeros((sh.rows, m))
+            st = O.FastPFP(p.A, p.Ap, p.B, p.Bp)
+            for t in range(6):
+                X_r, rho, sw = sharded_outer(sh, np.asarray(A_r, np.float64), np.asarray(Ap, np.float64),
+                                             K_r, X_r, Y_r, p.lam, p.alpha, 1e-7, 40, m)
+                Xo, rep = st.iterate(p.lam, p.alpha, 0.0, 1e-7, 1, 40)
+                assert np.max(np.abs(X_r - Xo[sh.sl])) < 1e-10, (n, npr, t)
+                assert abs(rho - rep.rho[0]) < 1e-10 and sw == rep.sweeps[0]
+        q.put((rank, "ok"))
+    except Exception as e:  # report to the parent
+        q.put((rank, repr(e)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_row_partition_rules():
+    sh = D.row_partition(16384, 16384, 8, 3)
+    assert (sh.row0, sh.rows) == (6144, 2048)
+    with pytest.raises(ValueError):
+        D.row_partition(1000, 1000, 8, 0)      # 125 rows per rank is not a multiple of 32
+    with pytest.raises(ValueError):
+        D.row_partition(800, 1000, 2, 0)       # n < n'
+    with pytest.raises(ValueError):
+        D.row_partition(64, 64, 2, 2)
+
+
+def test_sharded_decomposition_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

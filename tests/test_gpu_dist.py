@@ -1,0 +1,72 @@
+"""GPU tests of the row-sharded path (fastpfp_create_dist) at world size 1: the NCCL collectives
+(1-rank communicator), the 3-D TMA K-loop over gathered U blocks and the phase-split projection
+kernels all run; results must match the unsharded path and the fp64 oracle. (Multi-GPU runs use the
+same code with world > 1; the decomposition itself is checked with 2 gloo ranks on CPU.)"""
+import numpy as np
+import pytest
+
+from oracle import fastpfp as O
+from paper_1207_1114_b200 import inputs
+
+from .parity import X_TOL
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1207_1114_b200 as F
+    F.lib()
+
+
+def _dist_solver(p):
+    import paper_1207_1114_b200 as F
+    uid = F.nccl_unique_id()
+    return F.Solver(p.n, p.n_prime, p.d, dist=(0, 1, uid))
+
+
+def test_dist_world1_matches_single_and_oracle():
+    import paper_1207_1114_b200 as F
+    p = inputs.config5(n=2048)
+    a = F.Solver(p.n, p.n_prime, p.d)
+    a.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    b = _dist_solver(p)
+    b.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    st = O.FastPFP(p.A, p.Ap, p.B, p.Bp)
+    for t in range(4):
+        Xa, ra = a.iterate(p.alpha, p.lam, 0.0, 0.0, 1, 20)
+        Xb, rb = b.iterate(p.alpha, p.lam, 0.0, 0.0, 1, 20)
+        Xo, _ = st.iterate(p.lam, p.alpha, 0.0, 0.0, 1, 20)
+        assert rb.sweeps == [20]
+        assert np.max(np.abs(Xa - Xb)) <= 1e-6
+        assert np.max(np.abs(Xb.astype(np.float64) - Xo)) <= X_TOL
+    fo = O.objective(st.A, st.Ap, st.K, st.X, p.lam)
+    assert abs(b.objective(p.lam) - fo) <= 1e-4 * abs(fo)
+    assert np.array_equal(b.discretize(), O.greedy_discretize(st.X))
+
+
+@pytest.mark.parametrize("slack_mode", [0, 1])
+def test_dist_world1_slack_columns(slack_mode):
+    import paper_1207_1114_b200 as F
+    p = inputs.planted_unequal(77, 1024, 900, d=4, eps1=1e-5, eps2=1e-5, max_iter1=8, max_iter2=60)
+    s = _dist_solver(p)
+    s.set_option(F.OPT_SLACK_MODE, slack_mode)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    st = O.FastPFP(p.A, p.Ap, p.B, p.Bp, slack_mode="reset" if slack_mode else "persist")
+    for t in range(5):
+        X, r = s.iterate(p.alpha, p.lam, p.eps1, p.eps2, 1, p.max_iter2)
+        Xo, ro = st.iterate(p.lam, p.alpha, p.eps1, p.eps2, 1, p.max_iter2)
+        assert np.max(np.abs(X.astype(np.float64) - Xo)) <= X_TOL
+        assert abs(r.sweeps[0] - ro.sweeps[0]) <= 1
+
+
+def test_dist_rejects_unsupported_shapes():
+    import paper_1207_1114_b200 as F
+    uid = F.nccl_unique_id()
+    with pytest.raises(F.FastPFPError):
+        F.Solver(800, 1000, 0, dist=(0, 1, uid))     # n < n'
+    with pytest.raises(F.FastPFPError):
+        F.Solver(1000, 1000, 0, dist=(0, 1, uid))    # n/P not a multiple of 32
