@@ -250,3 +250,25 @@ def test_device_inputs_match_host_inputs():
     out = torch.empty((50, 70), dtype=torch.float32, device="cuda")
     b.copy_x(out)
     assert np.array_equal(out.cpu().numpy(), Xb)
+
+
+@pytest.mark.parametrize("shape", [(300, 200), (200, 300), (1000, 1000), (1, 9), (9, 1), (777, 513)])
+@pytest.mark.parametrize("kind", ["ties", "noisy_perm", "constant"])
+def test_gpu_greedy_equals_sequential_greedy(shape, kind):
+    # GPU locally-dominant rounds (+ host finish for tie chains) == Steps 1-3 of P:372-379
+    import paper_1207_1114_b200 as F
+    n, npr = shape
+    r = np.random.default_rng(n * 31 + npr)
+    if kind == "ties":
+        X = (np.round(r.random((n, npr)) * 7) / 7).astype(np.float32)
+    elif kind == "noisy_perm":
+        X = (r.random((n, npr)) * 0.1).astype(np.float32)
+        k = min(n, npr)
+        X[r.permutation(n)[:k], r.permutation(npr)[:k]] += 1.0
+    else:
+        X = np.full((n, npr), 0.25, np.float32)
+    s = F.Solver(n, npr, 0)
+    s.set_graphs(np.zeros((n, n), np.float32), np.zeros((npr, npr), np.float32))
+    s.set_x0(X)
+    a = s.discretize()
+    assert np.array_equal(a, O.greedy_discretize(X.astype(np.float64)))
