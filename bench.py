@@ -372,11 +372,14 @@ def secondary_c2(prec):
         res.append((solve_ms, wall, rep))
     solve_ms, wall, rep = sorted(res, key=lambda r: r[0])[len(res) // 2]
     acc = float((assign == p.perm).mean())
+    st = s.stats()
     s.close()
     return {"workload": workload_desc(p, "c2"), "value": round(rep.iterations / (solve_ms / 1e3), 3),
             "unit": UNIT, "outer_iterations": rep.iterations, "total_sweeps": rep.total_sweeps,
             "solve_ms": round(solve_ms, 3), "full_match_wall_ms": round(wall * 1e3, 3),
             "planted_recovery": acc, "ms_per_sweep": round(solve_ms / max(rep.total_sweeps, 1), 5),
+            "proj_kernel": ("on-chip tiles (%d CTAs, 1 grid barrier per sweep)" % st["onchip_tiles"]
+                            if st["onchip_launches"] else "streaming (2 grid barriers per sweep)"),
             "paper_context": "a few seconds for 1000-node graphs on a 3 GHz Core2 PC in MATLAB (PAPER.md:33-34)"}
 
 

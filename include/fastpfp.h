@@ -98,7 +98,11 @@ typedef enum fastpfp_option {
   FASTPFP_OPT_PROFILE = 6,
   /* tensor-core GEMM tiling: 2 (default) = 256 x 256 tiles per CTA pair (tcgen05 cta_group::2),
    * 1 = 128 x 128 tiles per CTA (cta_group::1). Same arithmetic, same results up to ordering. */
-  FASTPFP_OPT_GEMM_CTA_GROUP = 7
+  FASTPFP_OPT_GEMM_CTA_GROUP = 7,
+  /* projection kernel: 0 = auto (on-chip tiles with one grid barrier per sweep when Y fits in the
+   * aggregate shared memory, m <~ 2.2k; else streaming), 1 = streaming, 2 = on-chip (EUNSUPPORTED
+   * if Y does not fit). Same arithmetic; sums are reduced in a different fixed order. */
+  FASTPFP_OPT_PROJ_KERNEL = 8
 } fastpfp_option;
 
 /* Counters of a handle (since creation or the last fastpfp_reset_stats). */
@@ -111,6 +115,9 @@ typedef struct fastpfp_stats {
   double gemm_ms;            /* device time of GEMM launches (FASTPFP_OPT_PROFILE = 1)         */
   double proj_ms;            /* device time of projection launches (FASTPFP_OPT_PROFILE = 1)   */
   double gemm_flops;         /* algorithmic flops of the timed GEMM launches (2 M N K each)     */
+  int64_t onchip_launches;   /* of proj_launches, how many used the on-chip projection kernel  */
+  int32_t onchip_tiles;      /* PR * PC tiles of the on-chip kernel (0 if Y does not fit)      */
+  int32_t reserved;
 } fastpfp_stats;
 
 /* ---------------------------------------------------------------------------------------------

@@ -21,6 +21,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "fastpfp.h")
 OK, EINVAL, ESYM, ENONFINITE, ESTATE, ENOMEM, ECUDA, ENCCL, ENODEV, EPOISONED, EUNSUPPORTED = range(11)
 OPT_SLACK_MODE, OPT_PRECISION, OPT_RESCALE, OPT_STREAM, OPT_CHECK_EVERY, OPT_PROFILE = 1, 2, 3, 4, 5, 6
 OPT_GEMM_CTA_GROUP = 7
+OPT_PROJ_KERNEL = 8
 PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT = 0, 1, 2
 
 
@@ -44,7 +45,8 @@ class Stats(C.Structure):
     _fields_ = [
         ("launches", C.c_int64), ("gemm_launches", C.c_int64), ("proj_launches", C.c_int64),
         ("outer_iterations", C.c_int64), ("sweeps", C.c_int64), ("gemm_ms", C.c_double),
-        ("proj_ms", C.c_double), ("gemm_flops", C.c_double),
+        ("proj_ms", C.c_double), ("gemm_flops", C.c_double), ("onchip_launches", C.c_int64),
+        ("onchip_tiles", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

@@ -50,6 +50,13 @@ struct fastpfp_handle {
   double *sig_part = nullptr, *mu_part = nullptr;
   float *dlt_part = nullptr, *rho_part = nullptr;
   int TR = 8, RB = 1, CB = 1, RBx = 1, CBx = 1, grid = 1;
+  // on-chip projection (proj_onchip.cu)
+  bool oc_ok = false;
+  int proj_kernel = 0;   // FASTPFP_OPT_PROJ_KERNEL
+  int PR = 1, PC = 1, TRo = 1, TCo = 4;
+  double *oc_rowp = nullptr, *oc_colp = nullptr, *oc_tot = nullptr;
+  float* oc_dlt = nullptr;
+  unsigned* oc_bar = nullptr;
   DevIter* iters = nullptr;       // [kMaxCheck] device
   DevIter* h_iters = nullptr;     // pinned mirror
   int* done = nullptr;            // device flag
@@ -251,7 +258,9 @@ void fastpfp_destroy(fastpfp_handle* h) {
   if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
-                  (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal})
+                  (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal,
+                  (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
+                  (void*)h->oc_bar})
     if (p) cudaFree(p);
   if (h->h_iters) cudaFreeHost(h->h_iters);
   if (h->ev_ready)
@@ -305,6 +314,18 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
   A(alloc_arr(h->scal, 8));
+  if (!dist && onchip_fits((int)h->m, h->num_sms, h->PR, h->PC, h->TRo, h->TCo)) {
+    const int nb = h->PR * h->PC;
+    h->oc_ok = true;
+    A(alloc_arr(h->oc_rowp, 2 * (size_t)h->PC * M)); A(alloc_arr(h->oc_colp, 2 * (size_t)h->PR * M));
+    A(alloc_arr(h->oc_tot, 2 * (size_t)nb)); A(alloc_arr(h->oc_dlt, 2 * (size_t)nb));
+    A(alloc_arr(h->oc_bar, 1));
+    if (nb > h->grid) {   // mu/rho partials are indexed by tile
+      cudaFree(h->mu_part); cudaFree(h->rho_part);
+      h->mu_part = nullptr; h->rho_part = nullptr;
+      A(alloc_arr(h->mu_part, nb)); A(alloc_arr(h->rho_part, nb));
+    }
+  }
   A(cudaMallocHost(&h->h_iters, kMaxCheck * sizeof(DevIter)));
   A(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
@@ -378,6 +399,10 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
     case FASTPFP_OPT_GEMM_CTA_GROUP:
       if (value != 1 && value != 2) return FASTPFP_EINVAL;
       h->cta_group = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_PROJ_KERNEL:
+      if (value < 0 || value > 2) return FASTPFP_EINVAL;
+      if (value == 2 && !h->oc_ok) return set_err(h, FASTPFP_EUNSUPPORTED, "Y does not fit on chip");
+      h->proj_kernel = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_PROFILE:
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
       if (value && !h->ev_ready) {
@@ -654,6 +679,24 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
         h->stats.launches += 1;
       }
       // lines 4-9: projection loop, blend, rescale (one persistent kernel)
+      if (h->oc_ok && h->proj_kernel != 1) {
+        OnchipArgs oa{};
+        oa.Y = h->Y.p; oa.ldY = h->Y.ld; oa.m = (int)h->m;
+        oa.X = h->X.p; oa.Xb = h->Xb.p; oa.Xs = h->Xs.p; oa.ldX = h->X.ld; oa.n = N; oa.np = NP;
+        oa.alpha = alpha; oa.eps1 = eps1; oa.eps2 = eps2; oa.max_iter2 = max_iter2;
+        oa.rescale = h->rescale; oa.do_finalize = 1;
+        oa.PR = h->PR; oa.PC = h->PC; oa.TRo = h->TRo; oa.TCo = h->TCo;
+        oa.rowp = h->oc_rowp; oa.colp = h->oc_colp; oa.tot = h->oc_tot; oa.dlt = h->oc_dlt;
+        oa.mu_part = h->mu_part; oa.rho_part = h->rho_part; oa.iter_out = h->iters + k;
+        oa.done = h->done; oa.bar = h->oc_bar;
+        CK(h, cudaMemsetAsync(h->oc_bar, 0, sizeof(unsigned), s));
+        CK(h, launch_proj_onchip(oa, s));
+        h->stats.launches += 1;
+        h->stats.proj_launches += 1;
+        h->stats.onchip_launches += 1;
+        if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 2], s));
+        continue;
+      }
       ProjArgs pa{};
       pa.mode = kProjFull; pa.rows = (int)h->yrows;
       pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
@@ -714,6 +757,7 @@ int fastpfp_get_stats(fastpfp_handle* h, fastpfp_stats* out) {
   GUARD(h);
   if (!out) return FASTPFP_EINVAL;
   *out = h->stats;
+  out->onchip_tiles = h->oc_ok ? h->PR * h->PC : 0;
   return FASTPFP_OK;
 }
 

@@ -47,6 +47,28 @@ struct DevIter {
 // Arguments of the persistent projection + finalize kernel (proj.cu).
 enum ProjMode { kProjFull = 0, kProjSums = 1, kProjOneSweep = 2, kProjFinMu = 3, kProjFinApply = 4 };
 
+// On-chip projection (proj_onchip_kernel): the m x m Y is split into PR x PC tiles, one per CTA,
+// each resident in shared memory for the whole inner loop; one grid barrier per sweep.
+struct OnchipArgs {
+  float* Y; int64_t ldY; int m;
+  float* X; float* Xb; float* Xs; int64_t ldX; int n, np;
+  double alpha, eps1, eps2;
+  int max_iter2, rescale, do_finalize;
+  int PR, PC, TRo, TCo;          // tile grid and tile extent
+  double* rowp;                  // [2][PC][m] row partials
+  double* colp;                  // [2][PR][m] column partials
+  double* tot;                   // [2][PR*PC] tile totals
+  float* dlt;                    // [2][PR*PC] tile deltas
+  double* mu_part;               // [PR*PC]
+  float* rho_part;               // [PR*PC]
+  unsigned* bar;                 // exchange barrier counter (zeroed before each launch)
+  DevIter* iter_out;
+  int* done;
+};
+constexpr int kOnchipMaxTC = 256;
+cudaError_t launch_proj_onchip(const OnchipArgs& a, cudaStream_t s);
+bool onchip_fits(int m, int num_sms, int& PR, int& PC, int& TRo, int& TCo);
+
 struct ProjArgs {
   int mode;                                    // ProjMode (kProjFull: whole inner loop + finalize)
   float* Y; int64_t ldY; int m;                // slacked matrix, rows x m (row stride ldY, 16B rows)

@@ -33,12 +33,15 @@ class PairResult:
     X_oracle: np.ndarray
 
 
-def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=None, cta_group=2):
+def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=None, cta_group=2,
+             proj_kernel=0):
     from paper_1207_1114_b200 import (OPT_CHECK_EVERY, OPT_GEMM_CTA_GROUP, OPT_PRECISION, OPT_RESCALE,
                                       OPT_SLACK_MODE, Solver)
     s = Solver(p.n, p.n_prime, p.d)
     s.set_option(OPT_PRECISION, precision)
     s.set_option(OPT_GEMM_CTA_GROUP, cta_group)
+    from paper_1207_1114_b200 import OPT_PROJ_KERNEL
+    s.set_option(OPT_PROJ_KERNEL, proj_kernel)
     s.set_option(OPT_SLACK_MODE, slack_mode)
     s.set_option(OPT_RESCALE, rescale)
     if check_every:

@@ -86,11 +86,13 @@ def test_gemm_nt_error_bound(prec, cg, M, N, K):
 # ---------------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("prec", PRECS)
-def test_dyadic_two_node_bit_exact(golden_dir, prec):
+@pytest.mark.parametrize("pk", [pytest.param(0, id="auto-onchip"), pytest.param(1, id="streaming")])
+def test_dyadic_two_node_bit_exact(golden_dir, prec, pk):
     import paper_1207_1114_b200 as F
     g = json.load(open(os.path.join(golden_dir, "dyadic_two_node.json")))
     s = F.Solver(2, 2, 1)
     s.set_option(F.OPT_PRECISION, prec)
+    s.set_option(F.OPT_PROJ_KERNEL, pk)
     arr = lambda k: np.array(g[k], np.float32)
     s.set_graphs(arr("A"), arr("Ap"), arr("B"), arr("Bp"))
     s.set_x0(arr("X0"))
@@ -117,11 +119,12 @@ def test_config1_planted(prec):
 @pytest.mark.parametrize("shape", [(37, 53, 3), (53, 37, 3), (1, 1, 0), (1, 5, 2), (130, 129, 4),
                                    (60, 40, 4), (600, 520, 8)])
 @pytest.mark.parametrize("slack_mode", [0, 1])
-def test_ragged_planted_pairs(prec, shape, slack_mode):
+@pytest.mark.parametrize("pk", [pytest.param(0, id="auto-onchip"), pytest.param(1, id="streaming")])
+def test_ragged_planted_pairs(prec, shape, slack_mode, pk):
     # planted noisy subgraph pairs of both orientations (slack rows / slack columns, reading A1)
     n, npr, d = shape
     p = inputs.planted_unequal(17 + n + npr, n, npr, d=d)
-    res = run_pair(p, prec, slack_mode=slack_mode)
+    res = run_pair(p, prec, slack_mode=slack_mode, proj_kernel=pk)
     assert_parity(res)
 
 
@@ -147,17 +150,19 @@ def test_rescale_off(prec):
 
 
 @pytest.mark.parametrize("prec", PRECS)
-def test_config2_paper_scale(prec):
+@pytest.mark.parametrize("pk", [pytest.param(0, id="auto-onchip"), pytest.param(1, id="streaming")])
+def test_config2_paper_scale(prec, pk):
     p = inputs.config2()
-    res = run_pair(p, prec)
+    res = run_pair(p, prec, proj_kernel=pk)
     assert_parity(res, planted=p.perm)
     assert np.mean(res.assign_gpu == p.perm) >= 0.99
 
 
 @pytest.mark.parametrize("prec", PRECS)
-def test_config3_unequal_outliers(prec):
+@pytest.mark.parametrize("pk", [pytest.param(0, id="auto-onchip"), pytest.param(1, id="streaming")])
+def test_config3_unequal_outliers(prec, pk):
     p = inputs.config3()
-    res = run_pair(p, prec)
+    res = run_pair(p, prec, proj_kernel=pk)
     assert_parity(res)
 
 
