@@ -15,7 +15,7 @@ from typing import List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfastpfp.so")
+LIB_PATH = os.environ.get("FASTPFP_LIB") or os.path.join(HERE, "lib", "libfastpfp.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fastpfp.h")
 
 OK, EINVAL, ESYM, ENONFINITE, ESTATE, ENOMEM, ECUDA, ENCCL, ENODEV, EPOISONED, EUNSUPPORTED = range(11)

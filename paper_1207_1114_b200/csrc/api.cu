@@ -150,12 +150,12 @@ cudaError_t download(const Buf& b, float* dst, int is_device, cudaStream_t s) {
                            is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s);
 }
 
-// projection tiling: largest TR in {128, 64, 32, 16, 8} giving >= 2 tiles per SM, else 8
+// projection tiling: largest TR in {512, ..., 8} giving >= 2 tiles per SM, else 8
 void plan_projection(fastpfp_handle* h) {
   const int64_t m = h->m, rows = h->yrows;
   const int CB = (int)ceil_div(m, kProjTC);
   int TR = 8;
-  for (int tr : {128, 64, 32, 16, 8}) {
+  for (int tr : {512, 256, 128, 64, 32, 16, 8}) {
     if (ceil_div(rows, tr) * CB >= 2LL * h->num_sms) { TR = tr; break; }
   }
   h->TR = TR;

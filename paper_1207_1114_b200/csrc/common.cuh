@@ -94,7 +94,10 @@ struct ProjArgs {
 };
 
 constexpr int kProjThreads = 256;
-constexpr int kProjTC = 512;  // columns per projection tile (32 lanes x float4 x 4 chunks)
+#ifndef FPFP_PROJ_TC
+#define FPFP_PROJ_TC 256
+#endif
+constexpr int kProjTC = FPFP_PROJ_TC;  // columns per projection tile (32 lanes x float4 x TC/128 chunks)
 
 // host-side launchers (return cudaError_t)
 cudaError_t launch_proj(const ProjArgs& a, int grid, cudaStream_t s);

@@ -28,7 +28,10 @@ namespace fpfp {
 namespace {
 
 constexpr int kWarps = kProjThreads / kWarp;  // 8
-constexpr int kQ = kProjTC / 128;             // float4 chunks per lane per row (4)
+constexpr int kQ = kProjTC / 128;             // float4 chunks per lane per row
+#ifndef FPFP_PROJ_DEPTH
+#define FPFP_PROJ_DEPTH 2
+#endif
 
 struct __align__(16) ProjSmem {
   double col[kWarps][kProjTC];  // 32 KB: per-warp column partials of one tile
@@ -57,48 +60,82 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int j = j0 + e;
-      u[q][e] = (kSweep && j < p.m) ? p.c[j] * inv_m : 0.0;
+      u[q][e] = (kSweep && j < p.m) ? __ldcg(p.c + j) * inv_m : 0.0;
       colacc[q][e] = 0.0;
     }
   }
   const double tconst = (1.0 + sigma * inv_m) * inv_m;  // (1/n + 1^T Y 1 / n^2)
+  // this warp's rows are row0 + warp + 8 t, t < TR/8 <= 64: lane l holds r for t = l and t = l + 32
+  // (loaded up front, in parallel with the first rows of Y, then shuffled out row by row)
+  double r_lo = 0.0, r_hi = 0.0;
+  if (kSweep) {
+    const int ia = row0 + warp + kWarps * lane, ib = ia + kWarps * 32;
+    r_lo = ia < row1 ? __ldcg(p.r + ia) : 0.0;
+    r_hi = ib < row1 ? __ldcg(p.r + ib) : 0.0;
+  }
 
-  for (int i = row0 + warp; i < row1; i += kWarps) {
-    float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
-    float4 v[kQ];
+  // Software-pipelined over the warp's rows: a ring of kDepth rows of float4 loads stays in flight
+  // per thread (memory-level parallelism is what bounds this kernel), each slot refilled with the
+  // row kDepth steps ahead as soon as its own row has been corrected and stored.
+  constexpr int kDepth = FPFP_PROJ_DEPTH;
+  auto load_row = [&](int i, float4 (&v)[kQ]) {
+    const float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
 #pragma unroll
     for (int q = 0; q < kQ; ++q)
-      v[q] = inrow[q] ? *reinterpret_cast<const float4*>(rowp + q * 128) : make_float4(0, 0, 0, 0);
-    const double ti = kSweep ? tconst - p.r[i] * inv_m : 0.0;
-    double racc = 0.0;
+      v[q] = inrow[q] ? __ldcg(reinterpret_cast<const float4*>(rowp + q * 128)) : make_float4(0, 0, 0, 0);
+  };
+  float4 ring[kDepth][kQ];
+  const int i0 = row0 + warp;
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-      float* ve = reinterpret_cast<float*>(&v[q]);
+  for (int k = 0; k < kDepth; ++k)
+    if (i0 + k * kWarps < row1) load_row(i0 + k * kWarps, ring[k]);
+  for (int base = i0; base < row1; base += kDepth * kWarps) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = colbase + q * 128 + lane * 4 + e;
-        const bool valid = j < p.m;
-        const float y = ve[e];
-        float z = y;
-        if (kSweep) {
-          const double zd = ((double)y + ti) - u[q][e];          // P1, fp64
-          z = valid ? (float)fmax(zd, 0.0) : 0.0f;                // P2, one rounding to fp32
-          dmax = fmaxf(dmax, (float)fabs((double)z - (double)y)); // delta
-          ve[e] = z;
-        } else if (!valid) {
-          z = 0.0f;
-        }
-        racc += (double)z;
-        colacc[q][e] += (double)z;
+    for (int k = 0; k < kDepth; ++k) {
+      const int i = base + k * kWarps;
+      if (i >= row1) break;
+      float4 (&cur)[kQ] = ring[k];
+      float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
+      double ti = 0.0;
+      if (kSweep) {
+        const int t = (i - row0 - warp) / kWarps;
+        const double rlo = __shfl_sync(0xffffffffu, r_lo, t & 31);
+        const double rhi = __shfl_sync(0xffffffffu, r_hi, t & 31);
+        ti = tconst - (t < 32 ? rlo : rhi) * inv_m;
       }
-    }
-    if (kSweep) {
+      double racc = 0.0;
 #pragma unroll
-      for (int q = 0; q < kQ; ++q)
-        if (inrow[q]) *reinterpret_cast<float4*>(rowp + q * 128) = v[q];
+      for (int q = 0; q < kQ; ++q) {
+        float* ve = reinterpret_cast<float*>(&cur[q]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = colbase + q * 128 + lane * 4 + e;
+          const bool valid = j < p.m;
+          const float y = ve[e];
+          float z = y;
+          if (kSweep) {
+            const double zd = ((double)y + ti) - u[q][e];          // P1, fp64
+            z = valid ? (float)fmax(zd, 0.0) : 0.0f;                // P2, one rounding to fp32
+            dmax = fmaxf(dmax, fabsf(z - y));                       // delta
+            ve[e] = z;
+          } else if (!valid) {
+            z = 0.0f;
+          }
+          const double zz = (double)z;
+          racc += zz;
+          colacc[q][e] += zz;
+        }
+      }
+      if (kSweep) {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          if (inrow[q]) __stcg(reinterpret_cast<float4*>(rowp + q * 128), cur[q]);
+      }
+      const int ahead = i + kDepth * kWarps;
+      if (ahead < row1) load_row(ahead, ring[k]);
+      racc = warp_sum(racc);
+      if (lane == 0) p.rowpart[(int64_t)cb * p.rows + i] = racc;
     }
-    racc = warp_sum(racc);
-    if (lane == 0) p.rowpart[(int64_t)cb * p.rows + i] = racc;
   }
   // column partials of this tile: combine the 8 warps in a fixed order
 #pragma unroll

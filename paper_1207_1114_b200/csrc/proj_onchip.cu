@@ -23,7 +23,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxQ = kOnchipMaxTC / 32;   // columns per lane (8)
 
 struct OcShared {
   double colsum[kWarps][kOnchipMaxTC];

@@ -1,0 +1,12 @@
+#!/bin/bash
+# build a variant of libfastpfp.so with extra -D flags into build/var_<name>/ (experiments only)
+name=$1; shift
+out=build/var_$name; mkdir -p $out
+objs=""
+for f in paper_1207_1114_b200/csrc/*.cu; do
+  o=$out/$(basename $f).o
+  nvcc -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -gencode arch=compute_100a,code=sm_100a "$@" -c $f -o $o || exit 1
+  objs="$objs $o"
+done
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libfastpfp.so $objs -ldl
+echo built $out/libfastpfp.so
