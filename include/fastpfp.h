@@ -102,7 +102,11 @@ typedef enum fastpfp_option {
   /* projection kernel: 0 = auto (on-chip tiles with one grid barrier per sweep when Y fits in the
    * aggregate shared memory, m <~ 2.2k; else streaming), 1 = streaming, 2 = on-chip (EUNSUPPORTED
    * if Y does not fit). Same arithmetic; sums are reduced in a different fixed order. */
-  FASTPFP_OPT_PROJ_KERNEL = 8
+  FASTPFP_OPT_PROJ_KERNEL = 8,
+  /* 0 = FastPFP (Algorithm 1; default). 1 = Projected Gradient {pg}:
+   * X <- P_d(X + alpha (A X A' + lambda K)), same projection, initialisation and stopping rules,
+   * no blend and no rescale (alpha is the gradient step). SURVEY §8(f2). */
+  FASTPFP_OPT_METHOD = 9
 } fastpfp_option;
 
 /* Counters of a handle (since creation or the last fastpfp_reset_stats). */

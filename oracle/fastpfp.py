@@ -143,9 +143,14 @@ class Report:
 class FastPFP:
     """Algorithm 1 state machine: holds X and Y (slack persists across outer iterations unless
     slack_mode == 'reset', reading A3), so k calls of iterate(max_iter1=1) equal one call with
-    max_iter1=k (the C-ABI contract)."""
+    max_iter1=k (the C-ABI contract).
 
-    def __init__(self, A, Ap, B=None, Bp=None, X0=None, slack_mode="persist", rescale=True):
+    method = "fastpfp" (Algorithm 1, `{fastPFP}` P:206-211) or "pg", the Projected Gradient of
+    `{pg}`: X^(t+1) = P_d(X^(t) + alpha grad f(X^(t))) with the same slacked projection,
+    initialisation and stopping rules and no blend / rescale (reading A21)."""
+
+    def __init__(self, A, Ap, B=None, Bp=None, X0=None, slack_mode="persist", rescale=True,
+                 method="fastpfp"):
         self.A = np.asarray(A, F64)
         self.Ap = np.asarray(Ap, F64)
         self.n, self.n_prime = self.A.shape[0], self.Ap.shape[0]
@@ -155,6 +160,8 @@ class FastPFP:
         self.K = affinity(B, Bp, self.n, self.n_prime)
         self.slack_mode = slack_mode
         self.rescale = rescale
+        assert method in ("fastpfp", "pg")
+        self.method = method
         if X0 is None:
             # "X = 1 1^T_{n x n'} / n n', Y = 0_{n x n}" (Algorithm 1 line 1)
             X0 = np.ones((self.n, self.n_prime), dtype=F64) / (self.n * self.n_prime)
@@ -169,6 +176,13 @@ class FastPFP:
         G = gradient(self.A, self.Ap, self.K, self.X, lam)
         if self.slack_mode == "reset":
             self.Y = np.zeros((self.m, self.m), dtype=F64)
+        if self.method == "pg":
+            # {pg}: project X + alpha grad f; the projection output is the new X
+            self.Y[:n, :n_prime] = self.X + alpha * G
+            self.Y, sweeps, delta = project_loop(self.Y, eps2, max_iter2)
+            X_new = self.Y[:n, :n_prime].copy()
+            rho = float(np.max(np.abs(X_new - self.X)))
+            return X_new, rho, sweeps, delta, float(np.max(X_new))
         self.Y[:n, :n_prime] = G
         # lines 4-7: repeat P1, P2 until Y converges
         self.Y, sweeps, delta = project_loop(self.Y, eps2, max_iter2)
@@ -209,9 +223,10 @@ class FastPFP:
 
 
 def solve(problem, slack_mode="persist", rescale=True, trace_x=0, with_objective=False,
-          max_iter1=None):
-    """Run Algorithm 1 on an `inputs.Problem`. Returns (X, report, K)."""
-    st = FastPFP(problem.A, problem.Ap, problem.B, problem.Bp, problem.X0, slack_mode, rescale)
+          max_iter1=None, method="fastpfp"):
+    """Run Algorithm 1 (or PG) on an `inputs.Problem`. Returns (X, report, state)."""
+    st = FastPFP(problem.A, problem.Ap, problem.B, problem.Bp, problem.X0, slack_mode, rescale,
+                 method)
     X, rep = st.iterate(problem.lam, problem.alpha, problem.eps1, problem.eps2,
                         problem.max_iter1 if max_iter1 is None else max_iter1, problem.max_iter2,
                         trace_x=trace_x, with_objective=with_objective)

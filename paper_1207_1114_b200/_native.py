@@ -22,6 +22,8 @@ OK, EINVAL, ESYM, ENONFINITE, ESTATE, ENOMEM, ECUDA, ENCCL, ENODEV, EPOISONED, E
 OPT_SLACK_MODE, OPT_PRECISION, OPT_RESCALE, OPT_STREAM, OPT_CHECK_EVERY, OPT_PROFILE = 1, 2, 3, 4, 5, 6
 OPT_GEMM_CTA_GROUP = 7
 OPT_PROJ_KERNEL = 8
+OPT_METHOD = 9
+METHOD_FASTPFP, METHOD_PG = 0, 1
 PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT = 0, 1, 2
 
 

@@ -64,7 +64,7 @@ struct fastpfp_handle {
   double* scal = nullptr;         // device scalars (objective)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int slack_mode = 0, precision = 0, rescale = 1, check_every = 4, cta_group = 2;
+  int slack_mode = 0, precision = 0, rescale = 1, check_every = 4, cta_group = 2, method = 0;
   bool graphs_set = false, x0_custom = false, poisoned = false;
   int64_t t = 0;
   std::string err;
@@ -399,6 +399,9 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
     case FASTPFP_OPT_GEMM_CTA_GROUP:
       if (value != 1 && value != 2) return FASTPFP_EINVAL;
       h->cta_group = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_METHOD:
+      if (value != 0 && value != 1) return FASTPFP_EINVAL;
+      h->method = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_PROJ_KERNEL:
       if (value < 0 || value > 2) return FASTPFP_EINVAL;
       if (value == 2 && !h->oc_ok) return set_err(h, FASTPFP_EUNSUPPORTED, "Y does not fit on chip");
@@ -483,7 +486,8 @@ int fastpfp_reset(fastpfp_handle* h) {
 // ---- row-sharded outer iteration: every step is a local kernel; the three
 // exchanges are NCCL collectives on the handle's stream: all-gather of U's TF32 parts after GEMM1,
 // all-reduce SUM of [column sums | sigma] after every sweep, all-reduce MAX of mu and of rho.
-static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo, bool add_k) {
+static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo, bool add_k,
+                      double pg_alpha = 0.0) {
   cudaStream_t s = h->stream;
   const int N = (int)h->n, NP = (int)h->np;
   // U_r = A' X_r^T for the local rows r
@@ -505,9 +509,10 @@ static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo,
   g2.Qb = h->Uball.p; g2.Qs = h->Usall.p; g2.ldQ = h->Uball.ld;
   g2.M = N; g2.N = NP; g2.K = (int)h->n_glob;
   g2.q_blocks = h->world; g2.q_block_k = N; g2.q_block_stride = (int64_t)NP * h->Uball.ld;
-  g2.epi = kEpiAxpy; g2.C = out; g2.ldC = ldo;
+  g2.epi = (add_k && h->method == 1) ? kEpiPG : kEpiAxpy; g2.C = out; g2.ldC = ldo;
   g2.D = (add_k && lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
   g2.lam = (float)lambda;
+  g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)pg_alpha;
   return run_gemm(h, g2);
 }
 
@@ -530,7 +535,7 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
                       int32_t max_iter2, DevIter& out) {
   cudaStream_t s = h->stream;
   if (h->profile) CK(h, cudaEventRecord(h->ev[0], s));
-  int rc = dist_gemms(h, lambda, h->Y.p, h->Y.ld, true);
+  int rc = dist_gemms(h, lambda, h->Y.p, h->Y.ld, true, alpha);
   if (rc) return rc;
   if (h->profile) CK(h, cudaEventRecord(h->ev[1], s));
   if (h->slack_mode == 1 && h->m > h->np) {
@@ -539,7 +544,8 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
     h->stats.launches += 1;
   }
   const size_t mc = (size_t)h->m + 1;
-  ProjArgs pa = dist_proj_args(h, kProjSums, alpha, eps1, eps2);
+  ProjArgs pa = dist_proj_args(h, kProjSums, h->method == 1 ? 1.0 : alpha, eps1, eps2);
+  if (h->method == 1) pa.rescale = 0;
   CK(h, launch_proj(pa, h->grid, s));
   NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
   h->stats.launches += 1;
@@ -645,6 +651,9 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
   }
   CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
   const int N = (int)h->n, NP = (int)h->np;
+  // PG: the projection output is the new X (blend weight 1, no rescale)
+  const double blend = h->method == 1 ? 1.0 : alpha;
+  const int rescale = h->method == 1 ? 0 : h->rescale;
   int32_t left = max_iter1;
   bool stop = false;
   while (left > 0 && !stop) {
@@ -667,9 +676,10 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
       g2.Q = h->U.p; g2.ldQ = h->U.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
       g2.M = N; g2.N = NP; g2.K = N;
-      g2.epi = kEpiAxpy; g2.C = h->Y.p; g2.ldC = h->Y.ld;
+      g2.epi = h->method == 1 ? kEpiPG : kEpiAxpy; g2.C = h->Y.p; g2.ldC = h->Y.ld;
       g2.D = (lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
       g2.lam = (float)lambda;
+      g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;   // PG: X + alpha grad f
       g2.done = h->done;
       rc = run_gemm(h, g2);
       if (rc) return rc;
@@ -683,8 +693,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
         OnchipArgs oa{};
         oa.Y = h->Y.p; oa.ldY = h->Y.ld; oa.m = (int)h->m;
         oa.X = h->X.p; oa.Xb = h->Xb.p; oa.Xs = h->Xs.p; oa.ldX = h->X.ld; oa.n = N; oa.np = NP;
-        oa.alpha = alpha; oa.eps1 = eps1; oa.eps2 = eps2; oa.max_iter2 = max_iter2;
-        oa.rescale = h->rescale; oa.do_finalize = 1;
+        oa.alpha = blend; oa.eps1 = eps1; oa.eps2 = eps2; oa.max_iter2 = max_iter2;
+        oa.rescale = rescale; oa.do_finalize = 1;
         oa.PR = h->PR; oa.PC = h->PC; oa.TRo = h->TRo; oa.TCo = h->TCo;
         oa.rowp = h->oc_rowp; oa.colp = h->oc_colp; oa.tot = h->oc_tot; oa.dlt = h->oc_dlt;
         oa.mu_part = h->mu_part; oa.rho_part = h->rho_part; oa.iter_out = h->iters + k;
@@ -701,8 +711,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       pa.mode = kProjFull; pa.rows = (int)h->yrows;
       pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
       pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = N; pa.np = NP;
-      pa.alpha = alpha; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = max_iter2;
-      pa.rescale = h->rescale; pa.split = 1; pa.do_finalize = 1; pa.do_sums = 1;
+      pa.alpha = blend; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = max_iter2;
+      pa.rescale = rescale; pa.split = 1; pa.do_finalize = 1; pa.do_sums = 1;
       pa.TR = h->TR; pa.RB = h->RB; pa.CB = h->CB; pa.RBx = h->RBx; pa.CBx = h->CBx;
       pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c;
       pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;

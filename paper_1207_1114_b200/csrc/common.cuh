@@ -114,7 +114,7 @@ cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t 
                         int cols, double* out2, cudaStream_t s);
 
 // GEMM: C[M x N] = P[M x K] * Q[N x K]^T (+ epilogue). Both operands K-major.
-enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2 };
+enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2, kEpiPG = 3 };
 struct GemmArgs {
   const float* P; int64_t ldP;     // plain fp32 operands (SIMT path)
   const float* Q; int64_t ldQ;
@@ -126,6 +126,7 @@ struct GemmArgs {
   float* C2;                       // small part (kEpiSplit), ld = ldC
   float* C3;                       // optional plain copy in kEpiSplit (nullable), ld = ldC
   const float* D; int64_t ldD; float lam;  // kEpiAxpy: C = acc + lam * D
+  const float* D2; int64_t ldD2; float scale;  // kEpiPG: C = scale * (acc + lam * D) + D2
   const int* done;                 // nullable early-exit flag
   int cta_group = 2;               // tensor-core path: 1 = 128x128 tiles per CTA, 2 = 256x256 per CTA pair
   // row-sharded GEMM2: Q = [q_blocks][N][q_block_k] (one block per rank, block stride in floats)

@@ -84,6 +84,9 @@ __global__ void __launch_bounds__(256) gemm_nt_simt_kernel(GemmArgs g, bool vec_
       const int64_t o = (int64_t)gr * g.ldC + gc;
       if (g.epi == kEpiAxpy) {
         g.C[o] = g.D ? v + g.lam * g.D[(int64_t)gr * g.ldD + gc] : v;
+      } else if (g.epi == kEpiPG) {
+        const float gd = g.D ? v + g.lam * g.D[(int64_t)gr * g.ldD + gc] : v;
+        g.C[o] = g.scale * gd + g.D2[(int64_t)gr * g.ldD2 + gc];
       } else if (g.epi == kEpiSplit) {
         const float hb = tf32_rna(v);
         g.C[o] = hb;

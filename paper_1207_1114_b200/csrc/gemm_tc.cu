@@ -199,6 +199,7 @@ struct TcParams {
   int epi;
   float* C; float* C2; float* C3; int64_t ldC;
   const float* D; int64_t ldD; float lam;
+  const float* D2; int64_t ldD2; float scale;
   const int* done;
 };
 
@@ -391,7 +392,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
             }
           }
         } else {
-          const float* dd = (p.epi == kEpiAxpy && p.D) ? p.D + (int64_t)row * p.ldD + col0 : nullptr;
+          const float* dd = ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) ? p.D + (int64_t)row * p.ldD + col0 : nullptr;
+          const float* d2 = p.epi == kEpiPG ? p.D2 + (int64_t)row * p.ldD2 + col0 : nullptr;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             float4 o;
@@ -408,6 +410,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
                 if (dd && col0 + j + e < p.N) a += p.lam * dd[j + e];
                 oe[e] = a;
               }
+            }
+            if (d2) {   // Projected Gradient: X + alpha (A X A' + lambda K)
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (full || col0 + j + e < p.N) oe[e] = p.scale * oe[e] + d2[j + e];
             }
             if (full) {
               *reinterpret_cast<float4*>(c + j) = o;
@@ -499,7 +506,7 @@ cudaError_t launch_impl(const GemmArgs& g, cudaStream_t s, int device) {
     ok = ok && make_map(&mQb, g.Qb, g.N, g.K, g.ldQ) && make_map(&mQs, qs, g.N, g.K, g.ldQ);
   if (!ok) return cudaErrorInvalidValue;
   TcParams p{g.M, g.N, g.K, q3d ? 1 : 0, q3d ? g.q_block_k : 0, g.epi, g.C, g.C2, g.C3, g.ldC,
-             g.D, g.ldD, g.lam, g.done};
+             g.D, g.ldD, g.lam, g.D2, g.ldD2, g.scale, g.done};
   constexpr int kBoxes = PASSES == 1 ? 2 : 4;
   const size_t smem = (size_t)kStages * kBoxes * kBoxBytes + 1024;
   auto kern = gemm_tc_kernel<CG, PASSES>;

@@ -34,14 +34,15 @@ class PairResult:
 
 
 def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=None, cta_group=2,
-             proj_kernel=0):
+             proj_kernel=0, method=0):
     from paper_1207_1114_b200 import (OPT_CHECK_EVERY, OPT_GEMM_CTA_GROUP, OPT_PRECISION, OPT_RESCALE,
                                       OPT_SLACK_MODE, Solver)
     s = Solver(p.n, p.n_prime, p.d)
     s.set_option(OPT_PRECISION, precision)
     s.set_option(OPT_GEMM_CTA_GROUP, cta_group)
-    from paper_1207_1114_b200 import OPT_PROJ_KERNEL
+    from paper_1207_1114_b200 import OPT_METHOD, OPT_PROJ_KERNEL
     s.set_option(OPT_PROJ_KERNEL, proj_kernel)
+    s.set_option(OPT_METHOD, method)
     s.set_option(OPT_SLACK_MODE, slack_mode)
     s.set_option(OPT_RESCALE, rescale)
     if check_every:
@@ -49,7 +50,7 @@ def run_pair(p, precision, lockstep=10, slack_mode=0, rescale=1, check_every=Non
     s.set_graphs(p.A, p.Ap, p.B, p.Bp)
     s.set_x0(p.X0)
     st = O.FastPFP(p.A, p.Ap, p.B, p.Bp, p.X0, slack_mode="reset" if slack_mode else "persist",
-                   rescale=bool(rescale))
+                   rescale=bool(rescale), method="pg" if method == 1 else "fastpfp")
     lock = []
     g_iters = o_iters = 0
     g_sw, o_sw = [], []

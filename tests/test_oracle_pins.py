@@ -411,3 +411,37 @@ def test_planted_recovery_unweighted_e1():
         X, _, st = O.solve(p)
         ok += O.edge_error(st.A, st.Ap, O.greedy_discretize(X)) == 0.0
     assert ok >= 9
+
+
+# ---------------------------------------------------------------------------------------------
+# Projected Gradient {pg}, SURVEY §8(f2)
+# ---------------------------------------------------------------------------------------------
+
+def test_pg_dyadic_golden(golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "dyadic_pg.json")))
+    st = O.FastPFP(np.array(g["A"]), np.array(g["Ap"]), np.array(g["B"]), np.array(g["Bp"]),
+                   np.array(g["X0"]), method="pg")
+    for it in g["iters"]:
+        X, rep = st.iterate(g["lam"], g["alpha"], 0.0, g["eps2"], 1, g["max_iter2"])
+        assert np.array_equal(X, it["X"]) and rep.sweeps == [it["sweeps"]] and rep.rho == [it["rho"]]
+
+
+@pytest.mark.parametrize("n,npr", [(12, 8), (8, 12), (10, 10)])
+def test_pg_iterates_are_partial_doubly_stochastic(n, npr):
+    # every PG iterate is a P_d output, so it is partial DS at tight eps2
+    p = inputs.random_problem(31 + n, n, npr, d=2, lam=0.5, eps1=0.0, eps2=1e-13, max_iter1=6,
+                              max_iter2=200000)
+    st = O.FastPFP(p.A, p.Ap, p.B, p.Bp, method="pg")
+    for _ in range(6):
+        X, _ = st.iterate(p.lam, 0.01, 0.0, p.eps2, 1, p.max_iter2)
+        small, large = _smaller_larger_sums(X)
+        assert np.all(X >= -1e-9) and np.allclose(small, 1.0, atol=1e-9) and np.all(large <= 1 + 1e-9)
+
+
+def test_pg_zero_gradient_is_projection_fixed_point():
+    # A = A' = 0, lambda = 0: grad f = 0, so X1 = P_d(X0) and X2 = P_d(X1) = X1 (idempotence)
+    n = 7
+    st = O.FastPFP(np.zeros((n, n)), np.zeros((n, n)), method="pg")
+    X1, _ = st.iterate(0.0, 0.5, 0.0, 1e-14, 1, 100000)
+    X2, rep = st.iterate(0.0, 0.5, 0.0, 1e-14, 1, 100000)
+    assert np.allclose(X1, np.full((n, n), 1.0 / n), atol=1e-12) and rep.rho[0] < 1e-12
