@@ -4,6 +4,6 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl refere
 import this package. The product path never does.
 """
 from .fastpfp import (  # noqa: F401
-    FastPFP, Report, affinity, edge_error, gradient, greedy_discretize, greedy_discretize_literal,
+    FastPFP, Report, affinity, dykstra_project, edge_error, gradient, greedy_discretize, greedy_discretize_literal,
     objective, p1_affine, p2_nonneg, pd_project, project_loop, slack_embed, solve, sweep,
 )

@@ -121,6 +121,26 @@ def pd_project(X: np.ndarray, eps2: float, max_iter2: int):
     return Z[:n, :n_prime], sweeps, delta
 
 
+def dykstra_project(Y: np.ndarray, tol: float = 1e-12, max_iter: int = 100000):
+    """DIAGNOSTIC (reading A10): the exact Frobenius projection P_D(Y) of `{DSP}`
+     by Dykstra's alternating projection with correction terms between the affine set
+    {P1} and the cone {P2}. The paper's loop omits the corrections; with them the
+    iteration converges to the nearest doubly stochastic matrix. Not used by the method."""
+    Y = np.asarray(Y, F64)
+    X = Y.copy()
+    Pc = np.zeros_like(Y)      # correction for the affine step (affine sets need none, kept for form)
+    Qc = np.zeros_like(Y)      # correction for the cone step
+    for _ in range(max_iter):
+        Z = p1_affine(X + Pc)
+        Pc = X + Pc - Z
+        Xn = p2_nonneg(Z + Qc)
+        Qc = Z + Qc - Xn
+        if np.max(np.abs(Xn - X)) < tol:
+            return Xn
+        X = Xn
+    return X
+
+
 # ------------------------------------------------------------------------------------------------
 # Algorithm 1 (P:383-397) with the stopping rules of P:424-427
 # ------------------------------------------------------------------------------------------------

@@ -247,3 +247,60 @@ def stack_pairs(problems):
         B = np.ascontiguousarray(np.stack([p.B for p in problems]))
         Bp = np.ascontiguousarray(np.stack([p.Bp for p in problems]))
     return A, Ap, B, Bp
+
+
+# --------------------------------------------------------------------------------------------
+# fully connected Euclidean-distance graphs (the graph construction of the paper's
+# real-data experiments E2-E4: "each edge represents Euclidean distance between two keypoints",
+# PAPER.md:435; 128-d SIFT-like attributes with K_ij = inner products,
+# P:527-532). Synthetic stand-in: no dataset item is reproduced.
+# --------------------------------------------------------------------------------------------
+
+def _rotation(rng, dim):
+    Q, R = np.linalg.qr(rng.standard_normal((dim, dim)))
+    Q = Q * np.sign(np.diag(R))
+    if np.linalg.det(Q) < 0:
+        Q[:, 0] = -Q[:, 0]
+    return Q
+
+
+def _unit_rows(M):
+    M = np.abs(M)
+    return (M / np.maximum(np.linalg.norm(M, axis=1, keepdims=True), 1e-12)).astype(np.float32)
+
+
+def distance_pair(seed: int, n: int, n_outliers: int = 0, dim: int = 2, d: int = 128,
+                  jitter: float = 0.01, attr_noise: float = 0.05, lam: float = 1.0,
+                  alpha: float = 0.5, eps1: float = 1e-4, eps2: float = 1e-4, max_iter1: int = 300,
+                  max_iter2: int = 300) -> Problem:
+    """Points P in [0,1]^dim; the partner is a rigidly moved (rotation + translation), jittered,
+    permuted copy plus `n_outliers` uniform outlier points. A_ij = ||p_i - p_j|| (fully connected,
+    zero diagonal). Attributes: nonnegative unit 128-d vectors (SIFT-like), the
+    partner's inlier attributes perturbed by `attr_noise` and re-normalised; K = B B'^T (P:163).
+    n' = n + n_outliers >= n: slack rows (reading A1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    P = rng.random((n, dim))
+    R = _rotation(rng, dim)
+    Q_in = P @ R.T + rng.random(dim) + rng.standard_normal((n, dim)) * jitter
+    lo, hi = Q_in.min(0), Q_in.max(0)
+    Q_out = lo + rng.random((n_outliers, dim)) * (hi - lo)
+    Q = np.vstack([Q_in, Q_out])
+    npr = n + n_outliers
+    pi = rng.permutation(npr).astype(np.int64)
+    inv = np.empty_like(pi)
+    inv[pi] = np.arange(npr)
+    Qp = Q[inv]                                   # Q'[pi(i)] = Q[i]
+    dist = lambda X: np.sqrt(np.maximum(((X[:, None, :] - X[None, :, :]) ** 2).sum(-1), 0.0))
+    A = dist(P).astype(np.float32)
+    Ap = dist(Qp).astype(np.float32)
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(Ap, 0.0)
+    A = ((A + A.T) / 2).astype(np.float32)
+    Ap = ((Ap + Ap.T) / 2).astype(np.float32)
+    B = _unit_rows(rng.random((n, d)))
+    Bq = np.vstack([_unit_rows(B + rng.standard_normal((n, d)) * attr_noise),
+                    _unit_rows(rng.random((n_outliers, d)))])
+    Bp = np.ascontiguousarray(Bq[inv])
+    return Problem(f"dist{dim}d_{n}+{n_outliers}", A, Ap, B, Bp, lam=lam, alpha=alpha, eps1=eps1,
+                   eps2=eps2, max_iter1=max_iter1, max_iter2=max_iter2, perm=pi[:n].copy(), seed=seed,
+                   meta={"dim": dim, "jitter": jitter, "attr_noise": attr_noise})

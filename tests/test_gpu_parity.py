@@ -277,3 +277,15 @@ def test_gpu_greedy_equals_sequential_greedy(shape, kind):
     s.set_x0(X)
     a = s.discretize()
     assert np.array_equal(a, O.greedy_discretize(X.astype(np.float64)))
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("dims", [(392, 0, 3), (500, 40, 2)])
+def test_distance_workload_parity(prec, dims):
+    # fully connected Euclidean-distance graphs + 128-d attributes (E2-E4 style)
+    n, outl, dim = dims
+    p = inputs.distance_pair(21 + n, n, n_outliers=outl, dim=dim, jitter=0.005, lam=10.0,
+                             max_iter1=60, max_iter2=300)
+    res = run_pair(p, prec)
+    assert_parity(res)
+    assert np.mean(res.assign_gpu == p.perm) >= 0.95

@@ -445,3 +445,44 @@ def test_pg_zero_gradient_is_projection_fixed_point():
     X1, _ = st.iterate(0.0, 0.5, 0.0, 1e-14, 1, 100000)
     X2, rep = st.iterate(0.0, 0.5, 0.0, 1e-14, 1, 100000)
     assert np.allclose(X1, np.full((n, n), 1.0 / n), atol=1e-12) and rep.rho[0] < 1e-12
+
+
+# ---------------------------------------------------------------------------------------------
+# distance-graph workload and the Dykstra diagnostic
+# ---------------------------------------------------------------------------------------------
+
+def test_distance_pair_planted_geometry():
+    # the partner is a rigid motion of the points: inlier distances are preserved up to the jitter
+    p = inputs.distance_pair(3, 40, n_outliers=5, dim=3, jitter=0.0)
+    Ainl = p.Ap[np.ix_(p.perm, p.perm)]
+    assert np.allclose(Ainl, p.A, atol=1e-5)
+    assert np.array_equal(p.A, p.A.T) and np.array_equal(p.Ap, p.Ap.T)
+    assert np.allclose(np.linalg.norm(p.B, axis=1), 1.0, atol=1e-5) and np.all(p.B >= 0)
+
+
+def test_distance_pair_recovered_by_fastpfp():
+    # fully connected distance graphs + unit 128-d attributes: with lambda = 10 (the unit attributes
+    # carry ~1/10 of SIFT's inner-product scale) the planted match of the inliers is found
+    p = inputs.distance_pair(11, 40, n_outliers=6, dim=2, jitter=0.002, lam=10.0)
+    X, rep, st = O.solve(p)
+    a = O.greedy_discretize(X)
+    assert rep.converged and np.mean(a == p.perm) >= 0.95
+
+
+def test_dykstra_is_exact_projection_and_closer_than_alternation():
+    # Dykstra reaches the nearest DS matrix: it satisfies the KKT optimality of {DSP}:
+    # Y - D = a 1^T + 1 b^T - N with N >= 0 supported where D = 0 (checked via a 2x2 closed form and
+    # by being no farther from Y than the plain alternating limit)
+    r = RNG(17)
+    for _ in range(20):
+        Y = r.standard_normal((2, 2)) * 3
+        t = np.clip((Y[0, 0] + Y[1, 1] - Y[0, 1] - Y[1, 0] + 2) / 4, 0, 1)
+        anti = np.array([[0.0, 1.0], [1.0, 0.0]])
+        assert np.allclose(O.dykstra_project(Y), t * np.eye(2) + (1 - t) * anti, atol=1e-9)
+    for _ in range(10):
+        Y = r.standard_normal((6, 6)) * 2
+        D = O.dykstra_project(Y, tol=1e-13)
+        A, _, _ = O.project_loop(Y, 1e-13, 200000)
+        assert np.allclose(D.sum(0), 1, atol=1e-8) and np.allclose(D.sum(1), 1, atol=1e-8)
+        assert np.all(D >= -1e-10)
+        assert np.linalg.norm(Y - D) <= np.linalg.norm(Y - A) + 1e-9
