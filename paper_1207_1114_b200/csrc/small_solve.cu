@@ -114,6 +114,53 @@ __device__ __forceinline__ void gemm_acc(float (&acc)[8][8], const float (*Pres)
 
 namespace {
 
+// All 32 lanes hold partial sums v[0..15] of 16 rows; on return every lane holds the full sums.
+// Transpose-butterfly (each stage halves the values a lane carries: 8+4+2+1+1 shuffles) followed by
+// 16 broadcasts: 32 shuffles instead of 16 x 5. Fixed tree => deterministic.
+__device__ __forceinline__ void rows_allreduce16(float (&v)[16]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float a[8], b4[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float send = hi ? v[k] : v[8 + k], keep = hi ? v[8 + k] : v[k];
+      a[k] = keep + __shfl_xor_sync(F, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? a[k] : a[4 + k], keep = hi ? a[4 + k] : a[k];
+      b4[k] = keep + __shfl_xor_sync(F, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? b4[k] : b4[2 + k], keep = hi ? b4[2 + k] : b4[k];
+      b2[k] = keep + __shfl_xor_sync(F, send, 4);
+    }
+  }
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = keep + __shfl_xor_sync(F, send, 2);
+  }
+  b1 += __shfl_xor_sync(F, b1, 1);
+  // the lane with bits (16, 8, 4, 2) = (r3, r2, r1, r0) now holds row r = 8 r3 + 4 r2 + 2 r1 + r0
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int src = (((r >> 3) & 1) << 4) | (((r >> 2) & 1) << 3) | (((r >> 1) & 1) << 2) | ((r & 1) << 1);
+    v[r] = __shfl_sync(F, b1, src);
+  }
+}
+
+// kFull: n = n' = m = 128 (no bounds masks); kDelta: eps2 > 0 (the inner stop needs delta)
+template <bool kFull, bool kDelta>
 __global__ void __launch_bounds__(kT, 1) small_solve_kernel(SmallArgs p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SmallSmem& sm = *reinterpret_cast<SmallSmem*>(smem_raw);
@@ -186,8 +233,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_kernel(SmallArgs p) {
         // row partials (4 columns per lane) -> all-lane xor reduction per row
 #pragma unroll
         for (int r = 0; r < 16; ++r) rs[r] = (yy[r][0] + yy[r][1]) + (yy[r][2] + yy[r][3]);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) rs[r] = warp_sum(rs[r]);
+        rows_allreduce16(rs);
         // column partials over this warp's 16 rows
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -214,6 +260,9 @@ __global__ void __launch_bounds__(kT, 1) small_solve_kernel(SmallArgs p) {
         }
         const float sigma = warp_sum((cs[0] + cs[1]) + (cs[2] + cs[3]));
         const float tconst = (1.0f + sigma * inv_m) * inv_m;
+        float cu[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cu[e] = cs[e] * inv_m;
         buf ^= 1;
         dmax = 0.f;
 #pragma unroll
@@ -224,18 +273,22 @@ __global__ void __launch_bounds__(kT, 1) small_solve_kernel(SmallArgs p) {
           for (int e = 0; e < 4; ++e) {
             const int j = lane + 32 * e;
             const float yo = y[r][e];
-            const float z = (i < m && j < m) ? fmaxf((yo + ti) - cs[e] * inv_m, 0.f) : 0.f;  // P1, P2
-            dmax = fmaxf(dmax, fabsf(z - yo));
+            const float z = (kFull || (i < m && j < m)) ? fmaxf((yo + ti) - cu[e], 0.f) : 0.f;  // P1, P2
+            if (kDelta) dmax = fmaxf(dmax, fabsf(z - yo));
             y[r][e] = z;
           }
         }
         sums(y);
-        dmax = warp_max(dmax);
-        if (lane == 0) sm.dl[buf][warp] = dmax;
+        if (kDelta) {
+          dmax = warp_max(dmax);
+          if (lane == 0) sm.dl[buf][warp] = dmax;
+        }
         __syncthreads();
         delta = 0.f;
+        if (kDelta) {
 #pragma unroll
-        for (int w = 0; w < 8; ++w) delta = fmaxf(delta, sm.dl[buf][w]);
+          for (int w = 0; w < 8; ++w) delta = fmaxf(delta, sm.dl[buf][w]);
+        }
         ++s;
         if (delta < p.eps2 || s >= p.max_iter2) break;
       }
@@ -362,14 +415,13 @@ __global__ void __launch_bounds__(kT) small_greedy_kernel(const float* X, int ba
 size_t small_smem_bytes() { return sizeof(SmallSmem); }
 
 cudaError_t launch_small_solve(const SmallArgs& a, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(small_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(SmallSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  small_solve_kernel<<<grid, kT, sizeof(SmallSmem), s>>>(a);
+  const bool full = a.n == kS && a.np == kS;
+  const bool delta = a.eps2 > 0.0f;
+  void (*k)(SmallArgs) = full ? (delta ? small_solve_kernel<true, true> : small_solve_kernel<true, false>)
+                              : (delta ? small_solve_kernel<false, true> : small_solve_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSmem));
+  if (e != cudaSuccess) return e;
+  k<<<grid, kT, sizeof(SmallSmem), s>>>(a);
   return cudaGetLastError();
 }
 
