@@ -105,7 +105,13 @@ typedef enum fastpfp_option {
   FASTPFP_OPT_PROJ_KERNEL = 8,
   /* 0 = FastPFP (Algorithm 1; default). 1 = Projected Gradient {pg}:
    * X <- P_d(X + alpha (A X A' + lambda K)), same projection, initialisation and stopping rules,
-   * no blend and no rescale (alpha is the gradient step). SURVEY §8(f2). */
+   * no blend and no rescale (alpha is the gradient step). SURVEY §8(f2).
+   * 2 = FastGA (Appendix "FastGA", `{GAO3}`): per outer iteration
+   * X <- Sinkhorn(exp(beta_t (A X A' + lambda K))) on the slack-padded m x m matrix,
+   * beta_t = beta0 rate^t (fastpfp_set_ga_schedule); alpha is ignored; readings G1-G8 in DESIGN.md
+   * §3b. Single-GPU handles only (EUNSUPPORTED on a sharded handle). Allocates an m x m fp64
+   * workspace on first selection (ENOMEM if it does not fit). In the report, a FastGA iteration's
+   * "mu" entries carry beta_t and delta = +inf when only one Sinkhorn sweep ran. */
   FASTPFP_OPT_METHOD = 9
 } fastpfp_option;
 
@@ -133,6 +139,12 @@ typedef struct fastpfp_stats {
  * TF32 splits, K, X, Y (m x m), U, reduction scratch). *out is owned by the caller and released
  * with fastpfp_destroy. Errors: EINVAL (n, n' < 1, d < 0, out NULL), ENODEV, ENOMEM. */
 int fastpfp_create(int64_t n, int64_t n_prime, int64_t d, fastpfp_handle** out);
+
+/* FastGA annealing schedule (reading G5; the paper publishes none): outer iteration t
+ * uses beta_t = beta0 * rate^t, and fastpfp_iterate stops once beta_t > beta_max (t counts the
+ * handle's completed iterations since the last reset). Defaults 0.5, 1.075, 10. Errors: EINVAL
+ * unless beta0 > 0, rate >= 1, beta_max >= 0, all finite. */
+int fastpfp_set_ga_schedule(fastpfp_handle* h, double beta0, double rate, double beta_max);
 
 /* Load the graphs: A n x n, A_prime n' x n', B n x d, B_prime n' x d (B, B_prime may be
  * NULL iff d = 0). A and A' must be exactly symmetric (ESYM; not symmetrised) and finite

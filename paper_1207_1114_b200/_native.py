@@ -23,7 +23,7 @@ OPT_SLACK_MODE, OPT_PRECISION, OPT_RESCALE, OPT_STREAM, OPT_CHECK_EVERY, OPT_PRO
 OPT_GEMM_CTA_GROUP = 7
 OPT_PROJ_KERNEL = 8
 OPT_METHOD = 9
-METHOD_FASTPFP, METHOD_PG = 0, 1
+METHOD_FASTPFP, METHOD_PG, METHOD_FASTGA = 0, 1, 2
 PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT = 0, 1, 2
 
 
@@ -94,6 +94,7 @@ def lib():
         "fastpfp_nccl_unique_id": (C.c_int, [VP, I64]),
         "fastpfp_set_graphs": (C.c_int, [H, FP, FP, FP, FP, C.c_int]),
         "fastpfp_set_x0": (C.c_int, [H, FP, C.c_int]),
+        "fastpfp_set_ga_schedule": (C.c_int, [H, D, D, D]),
         "fastpfp_reset": (C.c_int, [H]),
         "fastpfp_iterate": (C.c_int, [H, D, D, D, D, I32, I32, FP, C.POINTER(Report)]),
         "fastpfp_copy_x": (C.c_int, [H, FP, C.c_int]),
@@ -236,6 +237,10 @@ class Solver:
 
     def reset(self):
         _check(lib().fastpfp_reset(self._h), self._h)
+
+    def set_ga_schedule(self, beta0=0.5, rate=1.075, beta_max=10.0):
+        _check(lib().fastpfp_set_ga_schedule(self._h, float(beta0), float(rate), float(beta_max)),
+               self._h)
 
     def iterate(self, alpha, lam, eps1, eps2, max_iter1, max_iter2, want_x=True, trace=None):
         trace = max_iter1 if trace is None else trace

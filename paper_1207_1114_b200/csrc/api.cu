@@ -57,6 +57,11 @@ struct fastpfp_handle {
   double *oc_rowp = nullptr, *oc_colp = nullptr, *oc_tot = nullptr;
   float* oc_dlt = nullptr;
   unsigned* oc_bar = nullptr;
+  // FastGA workspace (ga.cu), allocated on first use of FASTPFP_METHOD_FASTGA
+  double *ga_E = nullptr, *ga_u = nullptr, *ga_v = nullptr, *ga_dlt = nullptr, *ga_rho = nullptr;
+  int64_t ga_ldE = 0;
+  int ga_grid = 0, ga_W = 32;
+  double ga_beta0 = 0.5, ga_rate = 1.075, ga_beta_max = 10.0;  // reading G5 defaults
   DevIter* iters = nullptr;       // [kMaxCheck] device
   DevIter* h_iters = nullptr;     // pinned mirror
   int* done = nullptr;            // device flag
@@ -212,6 +217,21 @@ int check_flags(fastpfp_handle* h, const char* what) {
   return FASTPFP_OK;
 }
 
+// FastGA workspace: E (m x m fp64), u, v ([2][m] each), per-block partials
+int ga_alloc(fastpfp_handle* h) {
+  if (h->ga_E) return FASTPFP_OK;
+  h->ga_grid = ga_max_grid(h->device);
+  if (h->ga_grid < 1) return set_err(h, FASTPFP_ECUDA, "FastGA kernel cannot be made resident");
+  h->ga_W = ga_chunk_width((int)h->m, h->ga_grid);
+  h->ga_ldE = round_up(h->m, 32);
+  CK(h, alloc_arr(h->ga_E, (size_t)h->m * h->ga_ldE));
+  CK(h, alloc_arr(h->ga_u, 2 * (size_t)h->ga_ldE));
+  CK(h, alloc_arr(h->ga_v, 2 * (size_t)h->ga_ldE));
+  CK(h, alloc_arr(h->ga_dlt, h->ga_grid));
+  CK(h, alloc_arr(h->ga_rho, h->ga_grid));
+  return FASTPFP_OK;
+}
+
 }  // namespace
 
 int fpfp_discretize_device(fastpfp_handle*, const float*, int64_t, int, int, int32_t*,
@@ -260,7 +280,8 @@ void fastpfp_destroy(fastpfp_handle* h) {
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
                   (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal,
                   (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
-                  (void*)h->oc_bar})
+                  (void*)h->oc_bar, (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
+                  (void*)h->ga_dlt, (void*)h->ga_rho})
     if (p) cudaFree(p);
   if (h->h_iters) cudaFreeHost(h->h_iters);
   if (h->ev_ready)
@@ -400,7 +421,12 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
       if (value != 1 && value != 2) return FASTPFP_EINVAL;
       h->cta_group = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_METHOD:
-      if (value != 0 && value != 1) return FASTPFP_EINVAL;
+      if (value < 0 || value > 2) return FASTPFP_EINVAL;
+      if (value == 2) {
+        if (h->dist) return set_err(h, FASTPFP_EUNSUPPORTED, "FastGA is single-GPU only");
+        int rc = ga_alloc(h);
+        if (rc) return rc;
+      }
       h->method = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_PROJ_KERNEL:
       if (value < 0 || value > 2) return FASTPFP_EINVAL;
@@ -415,6 +441,15 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
       h->profile = (int)value; return FASTPFP_OK;
   }
   return set_err(h, FASTPFP_EINVAL, "unknown option key %d", key);
+}
+
+int fastpfp_set_ga_schedule(fastpfp_handle* h, double beta0, double rate, double beta_max) {
+  GUARD(h);
+  if (!(beta0 > 0.0) || !std::isfinite(beta0) || !(rate >= 1.0) || !std::isfinite(rate) ||
+      !(beta_max >= 0.0) || !std::isfinite(beta_max))
+    return set_err(h, FASTPFP_EINVAL, "beta0 > 0, rate >= 1, beta_max >= 0 (finite)");
+  h->ga_beta0 = beta0; h->ga_rate = rate; h->ga_beta_max = beta_max;
+  return FASTPFP_OK;
 }
 
 int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, const float* B,
@@ -655,6 +690,12 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
   const double blend = h->method == 1 ? 1.0 : alpha;
   const int rescale = h->method == 1 ? 0 : h->rescale;
   int32_t left = max_iter1;
+  if (h->method == 2) {   // FastGA anneals while beta_t = beta0 rate^t <= beta_max (reading G5)
+    int32_t allowed = 0;
+    while (allowed < left && h->ga_beta0 * std::pow(h->ga_rate, (double)(h->t + allowed)) <= h->ga_beta_max)
+      ++allowed;
+    left = allowed;
+  }
   bool stop = false;
   while (left > 0 && !stop) {
     const int chunk = std::min<int32_t>(left, h->check_every);
@@ -680,13 +721,28 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       g2.D = (lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
       g2.lam = (float)lambda;
       g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;   // PG: X + alpha grad f
-      g2.done = h->done;
+      g2.done = h->done;   // (FastGA: Y block = A X A' + lambda K, its exponent, reading G1)
       rc = run_gemm(h, g2);
       if (rc) return rc;
       if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 1], s));
-      if (h->slack_mode == 1 && h->m > std::min(h->n, h->np)) {
+      if (h->method != 2 && h->slack_mode == 1 && h->m > std::min(h->n, h->np)) {
         CK(h, launch_zero_slack(h->Y.p, h->Y.ld, (int)h->m, (int)h->m, N, NP, h->done, s));
         h->stats.launches += 1;
+      }
+      if (h->method == 2) {   // FastGA: exp + slack-padded Sinkhorn + X update (ga.cu)
+        GaArgs ga{};
+        ga.Q = h->Y.p; ga.ldQ = h->Y.ld; ga.m = (int)h->m; ga.n = N; ga.np = NP;
+        ga.beta = h->ga_beta0 * std::pow(h->ga_rate, (double)(h->t + k));   // reading G5
+        ga.eps1 = eps1; ga.eps2 = eps2; ga.max_iter2 = max_iter2; ga.W = h->ga_W;
+        ga.E = h->ga_E; ga.ldE = h->ga_ldE; ga.u = h->ga_u; ga.v = h->ga_v;
+        ga.dlt_part = h->ga_dlt; ga.rho_part = h->ga_rho;
+        ga.X = h->X.p; ga.Xb = h->Xb.p; ga.Xs = h->Xs.p; ga.ldX = h->X.ld;
+        ga.iter_out = h->iters + k; ga.done = h->done;
+        CK(h, launch_ga(ga, h->ga_grid, s));
+        h->stats.launches += 1;
+        h->stats.proj_launches += 1;
+        if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 2], s));
+        continue;
       }
       // lines 4-9: projection loop, blend, rescale (one persistent kernel)
       if (h->oc_ok && h->proj_kernel != 1) {

@@ -154,6 +154,25 @@ cudaError_t launch_small_solve(const SmallArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_small_greedy(const float* X, int batch, int n, int np, int32_t* assign, int grid,
                                 cudaStream_t s);
 
+// FastGA normalisation (ga.cu): stabilised exp of the GEMM output + slack-padded Sinkhorn + X
+// update, one cooperative kernel per outer iteration.
+struct GaArgs {
+  const float* Q; int64_t ldQ;   // exponent A X A' + lambda K on the n x n' block (Y buffer)
+  int m, n, np;
+  double beta, eps1, eps2;
+  int max_iter2;
+  int W;                         // pass-C column chunk width (8, 16 or 32)
+  double* E; int64_t ldE;        // m x m fp64 workspace
+  double* u; double* v;          // [2][ldE] each (sweep-parity double buffers)
+  double* dlt_part; double* rho_part;  // [grid]
+  float* X; float* Xb; float* Xs; int64_t ldX;
+  DevIter* iter_out;
+  int* done;
+};
+cudaError_t launch_ga(const GaArgs& a, int grid, cudaStream_t s);
+int ga_max_grid(int device);
+int ga_chunk_width(int m, int grid);
+
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t s, int device);
 bool gemm_tc_supported(const GemmArgs& g);

@@ -304,3 +304,26 @@ def distance_pair(seed: int, n: int, n_outliers: int = 0, dim: int = 2, d: int =
     return Problem(f"dist{dim}d_{n}+{n_outliers}", A, Ap, B, Bp, lam=lam, alpha=alpha, eps1=eps1,
                    eps2=eps2, max_iter1=max_iter1, max_iter2=max_iter2, perm=pi[:n].copy(), seed=seed,
                    meta={"dim": dim, "jitter": jitter, "attr_noise": attr_noise})
+
+
+def ga_pair(seed: int, n: int, n_prime: Optional[int] = None, p: float = 0.3, sigma_e: float = 0.02,
+            d: int = 0, lam: float = 0.0, q: float = 8.0, eps1: float = 1e-6, eps2: float = 1e-6,
+            max_iter1: int = 100, max_iter2: int = 100) -> Problem:
+    """FastGA workload: a planted noisy pair (config-1/2 recipe; when
+    n != n' the config-3 outlier recipe) whose edge weights are multiplied by
+    s = sqrt(q / (p n / 3)), so that the expected sum_j A_ij^2 is q whatever n is. GA's exponent
+    beta (A X A')_ia then peaks near beta_max * q at a permutation (about 80 with the defaults),
+    which keeps exp's argument well conditioned for an fp32 product. Sampling/scaling only."""
+    n_prime = n if n_prime is None else n_prime
+    if n_prime == n:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        A, Ap, B, Bp, pi = planted_pair(rng, n, p, sigma_e, d=d, sigma_b=0.1)
+    else:
+        base = planted_unequal(seed, n, n_prime, d=d, lam=lam)
+        A, Ap, B, Bp, pi = base.A, base.Ap, base.B, base.Bp, None
+    s = np.float32(np.sqrt(q / (p * max(n, n_prime) / 3.0)))
+    A = (A * s).astype(np.float32)
+    Ap = (Ap * s).astype(np.float32)
+    return Problem(f"ga_{n}x{n_prime}_d{d}", A, Ap, B, Bp, lam=lam if d > 0 else 0.0, alpha=0.0,
+                   eps1=eps1, eps2=eps2, max_iter1=max_iter1, max_iter2=max_iter2, perm=pi,
+                   seed=seed, meta={"weight_scale": float(s)})
