@@ -24,7 +24,7 @@ OPT_GEMM_CTA_GROUP = 7
 OPT_PROJ_KERNEL = 8
 OPT_METHOD = 9
 METHOD_FASTPFP, METHOD_PG, METHOD_FASTGA = 0, 1, 2
-PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT = 0, 1, 2
+PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT, PREC_INT8_OZAKI = 0, 1, 2, 3
 
 
 class FastPFPError(RuntimeError):

@@ -29,6 +29,14 @@ struct Buf {
   int rows = 0, cols = 0;
 };
 
+// Ozaki int8 form of a rows x K matrix: 3 digit planes (row stride ld bytes) + row exponents
+struct I8Buf {
+  int8_t* d[3] = {nullptr, nullptr, nullptr};
+  int64_t ld = 0;
+  int* e = nullptr;
+  int rows = 0, K = 0;
+};
+
 }  // namespace
 
 struct fastpfp_handle {
@@ -57,6 +65,10 @@ struct fastpfp_handle {
   double *oc_rowp = nullptr, *oc_colp = nullptr, *oc_tot = nullptr;
   float* oc_dlt = nullptr;
   unsigned* oc_bar = nullptr;
+  // Ozaki int8 operands (FASTPFP_OPT_PRECISION = 3, gemm_i8.cu), allocated on first use
+  I8Buf Ai8, Api8, Xi8, Ui8;
+  unsigned* Urowmax = nullptr;
+  bool i8_ready = false;
   // FastGA workspace (ga.cu), allocated on first use of FASTPFP_METHOD_FASTGA
   double *ga_E = nullptr, *ga_u = nullptr, *ga_v = nullptr, *ga_dlt = nullptr, *ga_rho = nullptr;
   int64_t ga_ldE = 0;
@@ -217,6 +229,95 @@ int check_flags(fastpfp_handle* h, const char* what) {
   return FASTPFP_OK;
 }
 
+cudaError_t alloc_i8(I8Buf& b, int rows, int K) {
+  b.rows = rows; b.K = K;
+  b.ld = round_up(std::max(K, 1), 128);
+  for (auto& d : b.d) {
+    cudaError_t e = alloc_arr(d, (size_t)std::max(rows, 1) * b.ld);
+    if (e != cudaSuccess) return e;
+  }
+  return alloc_arr(b.e, (size_t)std::max(rows, 1));
+}
+
+cudaError_t split_i8(const Buf& src, I8Buf& dst, const unsigned* rowmax, const int* done,
+                     cudaStream_t s) {
+  return launch_split_i8(src.p, src.ld, dst.rows, dst.K, rowmax, dst.d, dst.ld, dst.e, done, s);
+}
+
+// Ozaki int8 operands: allocate on first use and digit-split the constant graphs (A, A') and X
+int i8_prepare(fastpfp_handle* h) {
+  if (!h->i8_ready) {
+    if (!h->U.p) CK(h, alloc_buf(h->U, (int)h->np, (int)h->n));
+    CK(h, alloc_i8(h->Ai8, (int)h->n, (int)h->n_glob));
+    CK(h, alloc_i8(h->Api8, (int)h->np, (int)h->np));
+    CK(h, alloc_i8(h->Xi8, (int)h->n, (int)h->np));
+    CK(h, alloc_i8(h->Ui8, (int)h->np, (int)h->n));
+    CK(h, alloc_arr(h->Urowmax, (size_t)h->np));
+    h->i8_ready = true;
+  }
+  if (h->graphs_set) {
+    CK(h, split_i8(h->A, h->Ai8, nullptr, nullptr, h->stream));
+    CK(h, split_i8(h->Ap, h->Api8, nullptr, nullptr, h->stream));
+    CK(h, split_i8(h->X, h->Xi8, nullptr, nullptr, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
+  return FASTPFP_OK;
+}
+
+// The two products of Algorithm 1 line 3 on one GPU, in the handle's precision:
+// U = A' X^T (GEMM1), then out[0:n, 0:n'] = A U^T (+ lambda K when add_k; kEpiPG: X + alpha (...)).
+int run_products(fastpfp_handle* h, double lambda, float* out, int64_t ldo, int epi2, bool add_k,
+                 double alpha, const int* done) {
+  cudaStream_t s = h->stream;
+  const int N = (int)h->n, NP = (int)h->np;
+  if (h->precision == 3) {
+    CK(h, split_i8(h->X, h->Xi8, nullptr, done, s));   // digits of the current X
+    I8Gemm g1{};
+    for (int k = 0; k < 3; ++k) { g1.P[k] = h->Api8.d[k]; g1.Q[k] = h->Xi8.d[k]; }
+    g1.ldP = h->Api8.ld; g1.eP = h->Api8.e; g1.ldQ = h->Xi8.ld; g1.eQ = h->Xi8.e;
+    g1.M = NP; g1.N = N; g1.K = NP;
+    g1.epi = kEpiRowMax; g1.C = h->U.p; g1.ldC = h->U.ld; g1.rowmax = h->Urowmax; g1.done = done;
+    if (!gemm_i8_supported(g1)) return set_err(h, FASTPFP_EUNSUPPORTED, "int8 GEMM1 unsupported shape");
+    CK(h, cudaMemsetAsync(h->Urowmax, 0, (size_t)NP * sizeof(unsigned), s));
+    CK(h, launch_gemm_i8(g1, s, h->device));
+    CK(h, split_i8(h->U, h->Ui8, h->Urowmax, done, s));
+    I8Gemm g2{};
+    for (int k = 0; k < 3; ++k) { g2.P[k] = h->Ai8.d[k]; g2.Q[k] = h->Ui8.d[k]; }
+    g2.ldP = h->Ai8.ld; g2.eP = h->Ai8.e; g2.ldQ = h->Ui8.ld; g2.eQ = h->Ui8.e;
+    g2.M = N; g2.N = NP; g2.K = N;
+    g2.epi = epi2; g2.C = out; g2.ldC = ldo;
+    g2.D = (add_k && lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
+    g2.lam = (float)lambda;
+    g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;
+    g2.done = done;
+    CK(h, launch_gemm_i8(g2, s, h->device));
+    h->stats.launches += 4;
+    h->stats.gemm_launches += 2;
+    return FASTPFP_OK;
+  }
+  // U = A' X^T (= (X A')^T, A' symmetric) ...
+  GemmArgs g1{};
+  g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
+  g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
+  g1.M = NP; g1.N = N; g1.K = NP;
+  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->Ub.ld;
+  g1.C3 = h->precision == 2 ? h->U.p : nullptr;   // plain U only feeds the SIMT GEMM2
+  g1.done = done;
+  int rc = run_gemm(h, g1);
+  if (rc) return rc;
+  // ... then out = A U^T (+ lambda K) = A X A' + lambda K
+  GemmArgs g2{};
+  g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
+  g2.Q = h->U.p; g2.ldQ = h->Ub.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
+  g2.M = N; g2.N = NP; g2.K = N;
+  g2.epi = epi2; g2.C = out; g2.ldC = ldo;
+  g2.D = (add_k && lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
+  g2.lam = (float)lambda;
+  g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;   // PG: X + alpha grad f
+  g2.done = done;
+  return run_gemm(h, g2);
+}
+
 // FastGA workspace: E (m x m fp64), u, v ([2][m] each), per-block partials
 int ga_alloc(fastpfp_handle* h) {
   if (h->ga_E) return FASTPFP_OK;
@@ -275,6 +376,11 @@ void fastpfp_destroy(fastpfp_handle* h) {
   for (Buf* b : {&h->A, &h->Ab, &h->As, &h->Ap, &h->Apb, &h->Aps, &h->B, &h->Bp, &h->K, &h->X,
                  &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G, &h->Uball, &h->Usall})
     free_buf(*b);
+  for (I8Buf* b : {&h->Ai8, &h->Api8, &h->Xi8, &h->Ui8}) {
+    for (auto& d : b->d) if (d) cudaFree(d);
+    if (b->e) cudaFree(b->e);
+  }
+  if (h->Urowmax) cudaFree(h->Urowmax);
   if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
@@ -399,7 +505,12 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
       h->slack_mode = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_PRECISION:
-      if (value < 0 || value > 2) return FASTPFP_EINVAL;
+      if (value < 0 || value > 3) return FASTPFP_EINVAL;
+      if (value == 3) {
+        if (h->dist) return set_err(h, FASTPFP_EUNSUPPORTED, "int8 Ozaki GEMM is single-GPU only");
+        h->precision = 3;
+        return i8_prepare(h);
+      }
       h->precision = (int)value; return FASTPFP_OK;
     case FASTPFP_OPT_RESCALE:
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
@@ -493,6 +604,7 @@ int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, 
   rc = reset_state(h);
   if (rc) return rc;
   h->graphs_set = true;
+  if (h->precision == 3) return i8_prepare(h);   // digit planes of the new A, A'
   return FASTPFP_OK;
 }
 
@@ -702,27 +814,9 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
     CK(h, cudaMemsetAsync(h->iters, 0, chunk * sizeof(DevIter), s));
     for (int k = 0; k < chunk; ++k) {
       if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k], s));
-      // Algorithm 1 line 3: U = A' X^T (= (X A')^T, A' symmetric) ...
-      GemmArgs g1{};
-      g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
-      g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
-      g1.M = NP; g1.N = N; g1.K = NP;
-      g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->U.ld;
-      g1.C3 = h->precision == 2 ? h->U.p : nullptr;   // plain U only feeds the SIMT GEMM2
-      g1.done = h->done;
-      int rc = run_gemm(h, g1);
-      if (rc) return rc;
-      // ... then Y[0:n, 0:n'] = A U^T + lambda K = A X A' + lambda K
-      GemmArgs g2{};
-      g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
-      g2.Q = h->U.p; g2.ldQ = h->U.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
-      g2.M = N; g2.N = NP; g2.K = N;
-      g2.epi = h->method == 1 ? kEpiPG : kEpiAxpy; g2.C = h->Y.p; g2.ldC = h->Y.ld;
-      g2.D = (lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
-      g2.lam = (float)lambda;
-      g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;   // PG: X + alpha grad f
-      g2.done = h->done;   // (FastGA: Y block = A X A' + lambda K, its exponent, reading G1)
-      rc = run_gemm(h, g2);
+      // Algorithm 1 line 3: Y[0:n, 0:n'] = A X A' + lambda K (PG: X + alpha grad f)
+      int rc = run_products(h, lambda, h->Y.p, h->Y.ld, h->method == 1 ? kEpiPG : kEpiAxpy, true,
+                            alpha, h->done);
       if (rc) return rc;
       if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 1], s));
       if (h->method != 2 && h->slack_mode == 1 && h->m > std::min(h->n, h->np)) {
@@ -868,20 +962,7 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
     return FASTPFP_OK;
   }
   const int N = (int)h->n, NP = (int)h->np;
-  GemmArgs g1{};
-  g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
-  g1.Q = h->X.p; g1.ldQ = h->X.ld; g1.Qb = h->Xb.p; g1.Qs = h->Xs.p;
-  g1.M = NP; g1.N = N; g1.K = NP;
-  g1.epi = kEpiSplit; g1.C = h->Ub.p; g1.C2 = h->Us.p; g1.ldC = h->U.ld;
-  g1.C3 = h->precision == 2 ? h->U.p : nullptr;
-  int rc = run_gemm(h, g1);
-  if (rc) return rc;
-  GemmArgs g2{};
-  g2.P = h->A.p; g2.ldP = h->A.ld; g2.Pb = h->Ab.p; g2.Ps = h->As.p;
-  g2.Q = h->U.p; g2.ldQ = h->U.ld; g2.Qb = h->Ub.p; g2.Qs = h->Us.p;
-  g2.M = N; g2.N = NP; g2.K = N;
-  g2.epi = kEpiAxpy; g2.C = h->G.p; g2.ldC = h->G.ld; g2.D = nullptr;
-  rc = run_gemm(h, g2);
+  int rc = run_products(h, 0.0, h->G.p, h->G.ld, kEpiAxpy, false, 0.0, nullptr);
   if (rc) return rc;
   CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, N, NP, h->scal, s));
   double v[2];
@@ -963,7 +1044,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
 
 int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
                     int precision, int cta_group, int64_t stream) {
-  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || precision < 0 || precision > 2 ||
+  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || precision < 0 || precision > 3 ||
       (cta_group != 1 && cta_group != 2))
     return FASTPFP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -984,7 +1065,24 @@ int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t
     g.Q = Qp.p; g.ldQ = Qp.ld; g.Qb = Qb.p; g.Qs = Qs.p;
     g.M = (int)M; g.N = (int)N; g.K = (int)K; g.epi = kEpiPlain; g.C = Cp.p; g.ldC = Cp.ld;
     g.cta_group = cta_group;
-    if (precision == 2) {
+    if (precision == 3) {
+      I8Buf Pi, Qi;
+      A(alloc_i8(Pi, (int)M, (int)K)); A(alloc_i8(Qi, (int)N, (int)K));
+      if (rc == FASTPFP_OK) {
+        A(split_i8(Pp, Pi, nullptr, nullptr, s)); A(split_i8(Qp, Qi, nullptr, nullptr, s));
+        I8Gemm gi{};
+        for (int k = 0; k < 3; ++k) { gi.P[k] = Pi.d[k]; gi.Q[k] = Qi.d[k]; }
+        gi.ldP = Pi.ld; gi.eP = Pi.e; gi.ldQ = Qi.ld; gi.eQ = Qi.e;
+        gi.M = (int)M; gi.N = (int)N; gi.K = (int)K; gi.epi = kEpiPlain; gi.C = Cp.p; gi.ldC = Cp.ld;
+        if (!gemm_i8_supported(gi)) rc = FASTPFP_EUNSUPPORTED;
+        else A(launch_gemm_i8(gi, s, dev));
+      }
+      A(cudaStreamSynchronize(s));
+      for (I8Buf* b : {&Pi, &Qi}) {
+        for (auto& d : b->d) if (d) cudaFree(d);
+        if (b->e) cudaFree(b->e);
+      }
+    } else if (precision == 2) {
       A(launch_gemm_simt(g, s));
     } else if (!gemm_tc_supported(g)) {
       rc = FASTPFP_EUNSUPPORTED;

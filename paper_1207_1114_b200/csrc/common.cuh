@@ -114,7 +114,7 @@ cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t 
                         int cols, double* out2, cudaStream_t s);
 
 // GEMM: C[M x N] = P[M x K] * Q[N x K]^T (+ epilogue). Both operands K-major.
-enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2, kEpiPG = 3 };
+enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2, kEpiPG = 3, kEpiRowMax = 4 };
 struct GemmArgs {
   const float* P; int64_t ldP;     // plain fp32 operands (SIMT path)
   const float* Q; int64_t ldQ;
@@ -172,6 +172,26 @@ struct GaArgs {
 cudaError_t launch_ga(const GaArgs& a, int grid, cudaStream_t s);
 int ga_max_grid(int device);
 int ga_chunk_width(int m, int grid);
+
+// Ozaki int8 GEMM (gemm_i8.cu): C[M x N] = P Q^T with P, Q given as 3 int8 digit planes (row
+// stride ldP / ldQ bytes, K contiguous) and per-row power-of-two exponents eP / eQ.
+struct I8Gemm {
+  const int8_t* P[3]; int64_t ldP; const int* eP;
+  const int8_t* Q[3]; int64_t ldQ; const int* eQ;
+  int M, N, K;
+  int epi;                          // kEpiPlain, kEpiAxpy, kEpiPG or kEpiRowMax
+  float* C; int64_t ldC;
+  const float* D; int64_t ldD; float lam;
+  const float* D2; int64_t ldD2; float scale;
+  unsigned* rowmax;                 // kEpiRowMax: [M] |max| bits (zeroed by the caller)
+  const int* done;
+};
+bool gemm_i8_supported(const I8Gemm& g);
+cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device);
+// fp32 rows x K (stride lds floats) -> 3 digit planes (stride ldd bytes) + exponents; rowmax
+// (nullable) supplies max|row| bits, else it is computed.
+cudaError_t launch_split_i8(const float* src, int64_t lds, int rows, int K, const unsigned* rowmax,
+                            int8_t* const d[3], int64_t ldd, int* ex, const int* done, cudaStream_t s);
 
 cudaError_t launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs& g, int passes, cudaStream_t s, int device);

@@ -1,0 +1,414 @@
+// gemm_i8.cu — the two products of Algorithm 1 line 3, U = A' X^T and
+// Y[0:n,0:n'] = A U^T + lambda K, on the int8 tensor cores (tcgen05.mma.kind::i8) with an
+// Ozaki-style exact digit decomposition (FASTPFP_OPT_PRECISION = 3, DESIGN.md §6 "Ozaki int8").
+//
+// Every operand row r (K contiguous) is stored as a power-of-two scale 2^e_r and three signed
+// 7-bit digit planes:  x_rk = 2^e_r * (d1_rk 2^-7 + d2_rk 2^-14 + d3_rk 2^-21) + O(2^-22 2^e_r),
+// with e_r = frexp exponent of max_k |x_rk| (so |x / 2^e| < 1) and d_k = clamp(rint(r_k 128), +-127),
+// r_{k+1} = r_k 128 - d_k. The product of two such rows is
+//   sum_k P_ik Q_jk = 2^(eP_i + eQ_j) * sum_{p+q <= 4} 2^-7(p+q) (Dp_i . Dq_j)
+// where every digit dot product is an EXACT int32 (|d| <= 127, K <= 2^17 keeps |sum| < 2^31).
+// The six digit pairs fall into three weight classes w = p + q = 2, 3, 4, accumulated in three
+// int32 TMEM accumulators; the epilogue combines them in fp32 (2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)))
+// and applies the exact power-of-two scales. Dropped pairs (p + q >= 5) and the digit truncation
+// contribute <= 2^-21 relative to the row scales, the same order as an fp32 accumulation
+// (measured: tests/diagnostics/ozaki_drift.py, drift from the fp64 oracle equal to fp32's).
+//
+// Kernel shape: persistent, one CTA pair (cta_group::2) per 256 x 128 output tile; each CTA stages
+// 128 rows of P and 64 rows of Q per 128-byte K block (3 digit planes each, TMA SWIZZLE_128B,
+// 3-stage mbarrier ring, 72 KB per stage); one elected thread issues 6 x 4 UMMAs (K = 32 int8 each)
+// per stage; 3 x 128 TMEM columns hold the accumulators (single-buffered: 384 of 512 columns);
+// 4 epilogue warps read them with tcgen05.ld and apply the fused epilogue. The int8 pipe runs
+// 8192 MAC/clk/SM, 4x the TF32 rate, so 6 int8 MMAs cost half of 3xTF32's three TF32 MMAs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace fpfp {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kBKb = 128;                 // K bytes (int8 elements) per stage: one 128 B swizzle row
+constexpr int kPRows = 128;               // P rows per CTA
+constexpr int kQRows = 64;                // Q rows per CTA (N = 128 per pair)
+constexpr int kStages = 3;
+constexpr int kPBox = kPRows * kBKb;      // 16 KB
+constexpr int kQBox = kQRows * kBKb;      // 8 KB
+constexpr int kStageBytes = 3 * kPBox + 3 * kQBox;   // 72 KB
+constexpr int kThreads = 256;
+constexpr int kTileM = 256, kTileN = 128;
+constexpr uint32_t kTmemCols = 512;       // 3 x 128 used
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+struct I8Params {
+  int M, N, K;
+  const int* eP; const int* eQ;   // per-row exponents
+  int epi;
+  float* C; int64_t ldC;
+  const float* D; int64_t ldD; float lam;
+  const float* D2; int64_t ldD2; float scale;
+  unsigned* rowmax;               // kEpiRowMax: atomicMax of |C| bits per row (M side)
+  const int* done;
+};
+
+__device__ __forceinline__ void tile_coords_i8(int t, int num_m, int num_n, int& mt, int& nt) {
+  constexpr int kGroup = 8;
+  const int per_group = kGroup * num_n;
+  const int g = t / per_group;
+  const int first_m = g * kGroup;
+  const int gsz = min(num_m - first_m, kGroup);
+  const int r = t - g * per_group;
+  mt = first_m + r % gsz;
+  nt = r / gsz;
+}
+
+__device__ __forceinline__ float pow2f(int e) {
+  // exact 2^e for the normal range, ldexpf otherwise
+  return (e > -127 && e < 128) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ CUtensorMap mP2,
+               const __grid_constant__ CUtensorMap mP3, const __grid_constant__ CUtensorMap mQ1,
+               const __grid_constant__ CUtensorMap mQ2, const __grid_constant__ CUtensorMap mQ3,
+               I8Params p) {
+  if (p.done && *p.done) return;  // uniform across the grid
+
+  // D = S32, A = B = signed int8, K-major, N = 128, M = 256 (pair)
+  constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTileN >> 3) << 17) |
+                              ((uint32_t)(kTileM >> 4) << 24);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar;
+  __shared__ __align__(8) uint64_t tempty_bar;
+  __shared__ uint32_t tmem_base_sm;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int num_m = (int)ceil_div(p.M, kTileM), num_n = (int)ceil_div(p.N, kTileN);
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (int)ceil_div(p.K, kBKb);
+  const int cid = (int)cluster_id_x();
+  const int ncl = (int)num_clusters_x();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 4 * 2);
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sm)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sm;
+
+  if (warp == 0) {
+    // ===================== TMA producer (one elected lane per CTA) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        int mt, nt;
+        tile_coords_i8(t, num_m, num_n, mt, nt);
+        const int prow = mt * kTileM + (int)rank * kPRows;
+        const int qrow = nt * kTileN + (int)rank * kQRows;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          const uint32_t bar = mapa(smem_u32(&full_bar[stage]), 0);   // the leader's barrier
+          if (leader) mbar_expect_tx(&full_bar[stage], kStageBytes * 2);
+          const uint32_t base = smem_u32(smem + stage * kStageBytes);
+          const int kc = kb * kBKb;
+          tma_load<2>(&mP1, base + 0 * kPBox, bar, kc, prow);
+          tma_load<2>(&mP2, base + 1 * kPBox, bar, kc, prow);
+          tma_load<2>(&mP3, base + 2 * kPBox, bar, kc, prow);
+          tma_load<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kc, qrow);
+          tma_load<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kc, qrow);
+          tma_load<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kc, qrow);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one lane) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        mbar_wait(&tempty_bar, acc_phase ^ 1);   // epilogue drained the accumulators
+        tc_fence_after();
+        const uint32_t acc2 = tmem_base, acc3 = tmem_base + 128, acc4 = tmem_base + 256;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < kBKb / 32; ++k) {   // K = 32 int8 (32 bytes) per MMA
+            const uint32_t off = (uint32_t)k * 32u;
+            const uint64_t p1 = smem_desc(base + 0 * kPBox + off);
+            const uint64_t p2 = smem_desc(base + 1 * kPBox + off);
+            const uint64_t p3 = smem_desc(base + 2 * kPBox + off);
+            const uint64_t q1 = smem_desc(base + 3 * kPBox + 0 * kQBox + off);
+            const uint64_t q2 = smem_desc(base + 3 * kPBox + 1 * kQBox + off);
+            const uint64_t q3 = smem_desc(base + 3 * kPBox + 2 * kQBox + off);
+            const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
+            mma_i8(acc4, p3, q1, kIdesc, acc);   // weight 2^-28 class first
+            mma_i8(acc4, p2, q2, kIdesc, 1u);
+            mma_i8(acc4, p1, q3, kIdesc, 1u);
+            mma_i8(acc3, p2, q1, kIdesc, acc);   // 2^-21
+            mma_i8(acc3, p1, q2, kIdesc, 1u);
+            mma_i8(acc2, p1, q1, kIdesc, acc);   // 2^-14
+          }
+          umma_commit<2>(&empty_bar[stage]);     // frees the smem slot in both CTAs
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit<2>(&tfull_bar);              // accumulators ready (both CTAs)
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> registers -> global =====================
+    const int ew = warp & 3;
+    uint32_t acc_phase = 0;
+    const uint32_t tempty_leader = mapa(smem_u32(&tempty_bar), 0);
+    for (int t = cid; t < num_tiles; t += ncl) {
+      int mt, nt;
+      tile_coords_i8(t, num_m, num_n, mt, nt);
+      mbar_wait(&tfull_bar, acc_phase);
+      tc_fence_after();
+      const int row = mt * kTileM + (int)rank * kPRows + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+      const int eP = row_ok ? p.eP[row] : 0;
+      const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16);
+      float rmax = 0.0f;
+#pragma unroll 1
+      for (int cc = 0; cc < kTileN / 32; ++cc) {
+        uint32_t a2[32], a3[32], a4[32];
+        __syncwarp();
+        tmem_ld32(tb + (uint32_t)(cc * 32), a2);
+        tmem_ld32(tb + 128u + (uint32_t)(cc * 32), a3);
+        tmem_ld32(tb + 256u + (uint32_t)(cc * 32), a4);
+        if (cc == kTileN / 32 - 1) {   // all accumulator columns are in registers: release TMEM
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+        }
+        const int col0 = nt * kTileN + cc * 32;
+        if (!row_ok || col0 >= p.N) continue;
+        const bool full = col0 + 32 <= p.N;
+        float* c = p.C + (int64_t)row * p.ldC + col0;
+        const float* dd = ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) ? p.D + (int64_t)row * p.ldD + col0 : nullptr;
+        const float* d2 = p.epi == kEpiPG ? p.D2 + (int64_t)row * p.ldD2 + col0 : nullptr;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int col = col0 + j + e;
+            const bool ok = full || col < p.N;
+            const int eQ = ok ? __ldg(p.eQ + col) : 0;
+            // 2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)) * 2^(eP + eQ)
+            float v = fmaf((float)(int)a4[j + e], 0.0078125f, (float)(int)a3[j + e]);
+            v = fmaf(v, 0.0078125f, (float)(int)a2[j + e]);
+            v *= pow2f(eP + eQ - 14);
+            if (dd && ok) v += p.lam * dd[j + e];
+            if (d2 && ok) v = p.scale * v + d2[j + e];   // Projected Gradient
+            o[e] = v;
+            if (ok) rmax = fmaxf(rmax, fabsf(v));
+          }
+          if (full) {
+            *reinterpret_cast<float4*>(c + j) = make_float4(o[0], o[1], o[2], o[3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col0 + j + e < p.N) c[j + e] = o[e];
+          }
+        }
+      }
+      if (p.epi == kEpiRowMax && row_ok) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+      acc_phase ^= 1;
+    }
+  }
+
+  // teardown
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// ---- digit split: one warp per row ----------------------------------------------------------
+// rowmax (nullable): precomputed |max| bits per row (GEMM1's kEpiRowMax); else computed here.
+__global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int rows, int K,
+                                const unsigned* __restrict__ rowmax, int8_t* __restrict__ d1,
+                                int8_t* __restrict__ d2, int8_t* __restrict__ d3, int64_t ldd,
+                                int* __restrict__ ex, const int* done) {
+  if (done && *done) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  for (int r = gw; r < rows; r += nw) {
+    const float* x = src + (int64_t)r * lds;
+    float mx;
+    if (rowmax) {
+      mx = __uint_as_float(rowmax[r]);
+    } else {
+      mx = 0.0f;
+      for (int k = lane * 4; k < K; k += 128) {
+        if (k + 4 <= K) {
+          const float4 v = *reinterpret_cast<const float4*>(x + k);
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        } else {
+          for (int e = k; e < K; ++e) mx = fmaxf(mx, fabsf(x[e]));
+        }
+      }
+      mx = warp_max(mx);
+    }
+    int e = 0;
+    if (mx > 0.0f) frexpf(mx, &e);   // mx = f 2^e, f in [0.5, 1): |x / 2^e| < 1
+    if (lane == 0) ex[r] = e;
+    const float inv = ldexpf(1.0f, -e);
+    int8_t* o1 = d1 + (int64_t)r * ldd;
+    int8_t* o2 = d2 + (int64_t)r * ldd;
+    int8_t* o3 = d3 + (int64_t)r * ldd;
+    for (int k = lane * 4; k < K; k += 128) {
+      float v[4];
+      if (k + 4 <= K) {
+        const float4 q = *reinterpret_cast<const float4*>(x + k);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+      } else {
+        for (int t = 0; t < 4; ++t) v[t] = k + t < K ? x[k + t] : 0.0f;
+      }
+      char4 c1, c2, c3;
+      int8_t* p1 = reinterpret_cast<int8_t*>(&c1);
+      int8_t* p2 = reinterpret_cast<int8_t*>(&c2);
+      int8_t* p3 = reinterpret_cast<int8_t*>(&c3);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float r0 = v[t] * inv * 128.0f;                       // exact (power-of-two scaling)
+        const float a = fminf(fmaxf(rintf(r0), -127.0f), 127.0f);
+        float r1 = (r0 - a) * 128.0f;                         // exact remainder
+        const float b = fminf(fmaxf(rintf(r1), -127.0f), 127.0f);
+        const float r2 = (r1 - b) * 128.0f;
+        const float c = fminf(fmaxf(rintf(r2), -127.0f), 127.0f);
+        p1[t] = (int8_t)(int)a; p2[t] = (int8_t)(int)b; p3[t] = (int8_t)(int)c;
+      }
+      if (k + 4 <= K) {
+        *reinterpret_cast<char4*>(o1 + k) = c1;
+        *reinterpret_cast<char4*>(o2 + k) = c2;
+        *reinterpret_cast<char4*>(o3 + k) = c3;
+      } else {
+        for (int t = 0; t < 4 && k + t < K; ++t) { o1[k + t] = p1[t]; o2[k + t] = p2[t]; o3[k + t] = p3[t]; }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+std::once_flag g_enc_once;
+
+bool get_enc() {
+  std::call_once(g_enc_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_enc != nullptr;
+}
+
+// rows x K int8 plane with row stride ld bytes; box = box_rows x 128 bytes, SW128
+bool make_map_i8(CUtensorMap* m, const int8_t* base, int rows, int K, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gemm_i8_supported(const I8Gemm& g) {
+  if (!get_enc()) return false;
+  if (g.M < 1 || g.N < 1 || g.K < 1 || g.K > (1 << 17)) return false;
+  for (int k = 0; k < 3; ++k)
+    if (!g.P[k] || !g.Q[k] || (reinterpret_cast<uintptr_t>(g.P[k]) % 16) || (reinterpret_cast<uintptr_t>(g.Q[k]) % 16))
+      return false;
+  return (g.ldP % 16 == 0) && (g.ldQ % 16 == 0) && (g.ldC % 4 == 0) && g.eP && g.eQ;
+}
+
+cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  CUtensorMap mp[3], mq[3];
+  for (int k = 0; k < 3; ++k)
+    if (!make_map_i8(&mp[k], g.P[k], g.M, g.K, g.ldP, kPRows) || !make_map_i8(&mq[k], g.Q[k], g.N, g.K, g.ldQ, kQRows))
+      return cudaErrorInvalidValue;
+  I8Params p{g.M, g.N, g.K, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D, g.ldD, g.lam, g.D2, g.ldD2, g.scale,
+             g.rowmax, g.done};
+  const size_t smem = (size_t)kStages * kStageBytes + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int64_t tiles = ceil_div(g.M, kTileM) * ceil_div(g.N, kTileN);
+  const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel, mp[0], mp[1], mp[2], mq[0], mq[1], mq[2], p);
+}
+
+cudaError_t launch_split_i8(const float* src, int64_t lds, int rows, int K, const unsigned* rowmax,
+                            int8_t* const d[3], int64_t ldd, int* ex, const int* done, cudaStream_t s) {
+  const int warps = 8;
+  const int grid = (int)std::min<int64_t>(4096, std::max<int64_t>(1, ceil_div(rows, warps)));
+  split_i8_kernel<<<grid, warps * 32, 0, s>>>(src, lds, rows, K, rowmax, d[0], d[1], d[2], ldd, ex, done);
+  return cudaGetLastError();
+}
+
+}  // namespace fpfp

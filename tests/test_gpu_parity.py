@@ -28,7 +28,8 @@ def _need_gpu():
     F.lib()   # loud failure if the library is missing (no fallback)
 
 
-PRECS = [pytest.param(0, id="tf32x3"), pytest.param(2, id="simt")]  # PREC_TF32X3, PREC_FP32_SIMT
+PRECS = [pytest.param(0, id="tf32x3"), pytest.param(2, id="simt"),
+         pytest.param(3, id="int8ozaki")]  # PREC_TF32X3, PREC_FP32_SIMT, PREC_INT8_OZAKI
 
 
 # ---------------------------------------------------------------------------------------------
@@ -79,6 +80,36 @@ def test_gemm_nt_error_bound(prec, cg, M, N, K):
     bound = (K * 2.0**-24 + 3 * 2.0**-22) * mag + 1e-30
     err = np.abs(C.cpu().numpy().astype(np.float64) - exact)
     assert np.all(err <= bound), float(np.max(err / bound))
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (129, 257, 33), (300, 1000, 700),
+                                   (1000, 1000, 1000), (256, 512, 4096), (1500, 700, 2048),
+                                   (640, 384, 16384)])
+@pytest.mark.parametrize("signed", [False, True])
+def test_gemm_nt_int8_ozaki_error_bound(M, N, K, signed):
+    # Ozaki int8 (PRECISION = 3): rows = 2^e * (3 signed 7-bit digits), digit pairs p + q <= 4
+    # exact in int32. Per element: representation error <= 2^-21 of the row scale per operand entry,
+    # dropped pairs (p + q >= 5, remainder digits |d| <= 64) <= 2^-22 s_P s_Q per k, fp32 combine
+    # <= 2^-22 |P||Q|^T
+    import paper_1207_1114_b200 as F
+    r = np.random.default_rng(M * 5 + N * 11 + K + signed)
+    P = (r.random((M, K)) * (r.random((M, K)) < 0.5)).astype(np.float32)
+    Q = r.random((N, K)).astype(np.float32) * np.float32(1e-3)
+    if signed:
+        P = (P - np.float32(0.25) * (P > 0)).astype(np.float32)
+        Q = (Q * np.where(r.random((N, K)) < 0.5, -1, 1)).astype(np.float32)
+    C = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    F.gemm_nt(torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda(), C, F.PREC_INT8_OZAKI, 2)
+    P64, Q64 = P.astype(np.float64), Q.astype(np.float64)
+    exact = P64 @ Q64.T
+    scale = lambda M_: np.exp2(np.floor(np.log2(np.maximum(np.max(np.abs(M_), 1), 1e-300))) + 1)
+    sP, sQ = scale(P64), scale(Q64)
+    rep = 2.0**-21 * (np.abs(P64).sum(1)[:, None] * sQ[None, :] + sP[:, None] * np.abs(Q64).sum(1)[None, :])
+    bound = rep + K * 2.0**-22 * sP[:, None] * sQ[None, :] + 2.0**-22 * (np.abs(P64) @ np.abs(Q64).T) + 1e-30
+    err = np.abs(C.cpu().numpy().astype(np.float64) - exact)
+    assert np.all(err <= bound), float(np.max(err / bound))
+    # and it is far more accurate than 1xTF32 (2^-11) on these inputs
+    assert np.max(err / (np.abs(P64) @ np.abs(Q64).T + 1e-30)) < 2.0**-16
 
 
 # ---------------------------------------------------------------------------------------------
@@ -167,7 +198,7 @@ def test_config3_unequal_outliers(prec, pk):
 
 
 @pytest.mark.parametrize("prec,cg", [pytest.param(0, 2, id="tf32x3"), pytest.param(0, 1, id="tf32x3-cg1"),
-                                     pytest.param(2, 2, id="simt")])
+                                     pytest.param(2, 2, id="simt"), pytest.param(3, 2, id="int8ozaki")])
 def test_config5_recipe_reduced(prec, cg):
     # the c5 recipe (p = 0.1, d = 64, lambda = 1, fixed 20 x 20) at n = 2048: spans 8 x 8 pair tiles
     # of the GEMM and 4 x 16 projection tile columns, exercised by the oracle in seconds

@@ -13,7 +13,7 @@ from .parity import run_pair
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-PRECS = [pytest.param(0, id="tf32x3"), pytest.param(2, id="simt")]
+PRECS = [pytest.param(0, id="tf32x3"), pytest.param(2, id="simt"), pytest.param(3, id="int8ozaki")]
 PKS = [pytest.param(0, id="auto"), pytest.param(1, id="streaming")]
 
 
