@@ -158,7 +158,7 @@ def proj_bytes_per_outer(n, npr, sweeps):
 
 
 def precision_name(prec):
-    return {0: "tf32x3", 1: "tf32", 2: "fp32_simt"}[prec]
+    return {0: "tf32x3", 1: "tf32", 2: "fp32_simt", 3: "int8_ozaki"}[prec]
 
 
 def gemm_peak(mp, src, prec):
@@ -167,6 +167,12 @@ def gemm_peak(mp, src, prec):
     so its algorithmic-flop peak is a third of that. SIMT fp32: 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
     if prec == 2:
         return 148 * 128 * 2 * 1.965e9 / 1e12, "alu", f"fp32 FFMA peak 74.4 TF/s (148 SMs x 128 lanes x 2 flop x 1.965 GHz, derived)"
+    if prec == 3:
+        # the GEMM runs inside a long step: sustained figure (B200_PROFILING.md)
+        i8 = mp["bf16_tflops_sustained"] * 2.0
+        return i8 / 6.0, "tensor", (f"int8 Ozaki: ({src} bf16 sustained {mp['bf16_tflops_sustained']} x 4.5/2.25 "
+                                    f"nominal int8/bf16 dense ratio = {i8:.0f} TOPS) / 6 int8 MMAs per "
+                                    f"fp32-accurate product")
     tf32 = mp["bf16_tflops"] * (1.1 / 2.25)
     if prec == 1:
         return tf32, "tensor", f"tf32 = {src} bf16 burst {mp["bf16_tflops"]} x 1.1/2.25 (nominal dense ratio)"
@@ -296,6 +302,7 @@ def run_ours(args):
         out["secondary"] = secondary_c2(prec)
         out["secondary_c4"] = secondary_c4()
         out["secondary_pg"] = secondary_c2(prec, method=1)
+        out["secondary_fastga"] = secondary_ga(prec)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.workload, steps=2)
     s.close()
@@ -341,6 +348,47 @@ def e2e(s, p, inner, stream, world, shard=None):
             "what": f"fastpfp_set_graphs(pinned host A,A',B,B') + set_x0 + iterate({outer} outer x {inner} sweeps) "
                     f"+ fastpfp_copy_x(pinned host); bytes amortised over the {outer} outer steps of one solve",
             "ms_per_solve": round(ms, 3)}
+
+
+def secondary_ga(prec):
+    """FastGA at n = 1000 on the GA-scaled c2 recipe (inputs.ga_pair):
+    full annealing run (beta 0.5 x 1.075^t <= 10, eps = 1e-4, <= 100 Sinkhorn sweeps) + greedy,
+    next to FastPFP's c2 solve (the paper's speed comparison)."""
+    import torch
+
+    import paper_1207_1114_b200 as F
+    from paper_1207_1114_b200 import inputs
+    p = inputs.ga_pair(2, 1000, d=32, lam=1.0, p=0.5, sigma_e=0.05, eps1=1e-4, eps2=1e-4,
+                       max_iter1=300, max_iter2=100)
+    s = F.Solver(p.n, p.n_prime, p.d)
+    stream = torch.cuda.current_stream()
+    s.set_option(F.OPT_STREAM, stream.cuda_stream)
+    s.set_option(F.OPT_PRECISION, prec)
+    s.set_option(F.OPT_CHECK_EVERY, 8)
+    s.set_option(F.OPT_METHOD, F.METHOD_FASTGA)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    res = []
+    for _ in range(3):
+        s.reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = s.iterate(0.0, p.lam, p.eps1, p.eps2, p.max_iter1, p.max_iter2, want_x=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solve_ms = e0.elapsed_time(e1)
+        assign = s.discretize()
+        res.append((solve_ms, (time.perf_counter() - t0) * 1e3, rep))
+    solve_ms, wall_ms, rep = sorted(res, key=lambda r: r[0])[1]
+    s.close()
+    return {"workload": "FastGA (Appendix {GAO3} + slack-padded Sinkhorn) on the c2 recipe with GA-scaled "
+                        "weights, n=n'=1000, d=32, lambda=1, beta=0.5*1.075^t<=10, eps=1e-4, I1<=100",
+            "value": round(rep.iterations / (solve_ms / 1e3), 3), "unit": UNIT,
+            "outer_iterations": rep.iterations, "total_sweeps": rep.total_sweeps,
+            "solve_ms": round(solve_ms, 3), "full_match_wall_ms": round(wall_ms, 3),
+            "ms_per_sweep": round(solve_ms / max(rep.total_sweeps, 1), 5),
+            "planted_recovery": float((assign == p.perm).mean())}
 
 
 def secondary_c2(prec, method=0):
@@ -494,7 +542,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c5", "c2"])
-    ap.add_argument("--precision", type=int, default=int(os.environ.get("FASTPFP_BENCH_PRECISION", "0")))
+    ap.add_argument("--precision", type=int, default=int(os.environ.get("FASTPFP_BENCH_PRECISION", "3")))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
