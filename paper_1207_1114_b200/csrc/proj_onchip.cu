@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -21,7 +22,10 @@ namespace cg = cooperative_groups;
 namespace fpfp {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef FPFP_OC_THREADS
+#define FPFP_OC_THREADS 256
+#endif
+constexpr int kThreads = FPFP_OC_THREADS;
 constexpr int kWarps = kThreads / 32;
 
 struct OcShared {
@@ -39,7 +43,10 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   cg::grid_group grid = cg::this_grid();
   // The tile is held in fp64 on chip (no per-sweep rounding: closer to the fp64 definition than
   // the streaming kernel's fp32 storage); it is rounded to fp32 once, when written back.
-  extern __shared__ __align__(16) double tile[];   // [TRo][TCo]
+  // Rows of the shared tile are padded to kLdt = 32 NQ columns: padded entries are 0 and their
+  // column correction is +1e300, so P2 keeps them at 0 and the element loop needs no bounds test.
+  constexpr int kLdt = 32 * NQ;
+  extern __shared__ __align__(16) double tile[];   // [TRo][kLdt]
   __shared__ OcShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x;
@@ -52,76 +59,105 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 
   // load the tile
   for (int i = warp; i < nr; i += kWarps)
-    for (int j = lane; j < nc; j += 32) tile[i * p.TCo + j] = (double)p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j];
+    for (int j = lane; j < kLdt; j += 32)
+      tile[i * kLdt + j] = j < nc ? (double)p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] : 0.0;
   __syncthreads();
 
   // One fused pass over the tile: optionally apply the sweep (P1 then P2, fp64 correction, one
   // rounding), and emit the fp64 row / column partial sums, the tile total and the tile delta of
-  // the resulting values to exchange buffer `buf`. Rows are processed 4 at a time so the 4 warp
-  // reductions interleave (latency, not bandwidth, bounds this kernel).
+  // the resulting values to exchange buffer `buf`. Latency, not bandwidth, bounds this kernel at
+  // n ~ 1000, so the element loop carries no cross-lane reduction and no fp64
+  // max chain: warp w walks rows w, w+8, ...; lane l keeps its columns' partial sums in registers
+  // and writes its per-row partial to shared memory (rowacc[i][l]); the 32 lane partials of a row
+  // and the 8 warp partials of a column are then summed by one thread each, in a fixed order.
+  // P2 is a sign test (max(z, 0) for finite z), the delta is tracked in fp32: rounding is
+  // monotonic, so max_ij fl32(|dz|) = fl32(max_ij |dz|), the same value the fp64 max would give.
+  double* rowacc = tile + (size_t)p.TRo * kLdt;   // [TRo][33]
+#ifdef FPFP_OC_PROF
+  long long pc_rows = 0, pc_cols = 0;
+#endif
   auto pass = [&](bool update, int buf, double tconst) {
-    double cacc[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) cacc[q] = 0.0;
-    double tacc = 0.0;
-    double dmax = 0.0;
-    double cj[NQ];
+#ifdef FPFP_OC_PROF
+    const long long c0_ = clock64();
+#endif
+    double cacc[NQ], cj[NQ];
+    float dq[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
+      cacc[q] = 0.0;
+      dq[q] = 0.0f;
       const int j = lane + 32 * q;
-      cj[q] = (update && j < nc) ? sh.c[j] * inv_m : 0.0;
+      cj[q] = j < nc ? sh.c[j] * inv_m : 1e300;
     }
-    for (int i0 = warp * 4; i0 < nr; i0 += kWarps * 4) {
-      double racc[4];
+    if (update) {
+#pragma unroll 2
+      for (int i = warp; i < nr; i += kWarps) {
+        const double ti = tconst - sh.r[i] * inv_m;
+        double* row = &tile[i * kLdt + lane];
+        double y[NQ], z[NQ];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        racc[u] = 0.0;
-        const int i = i0 + u;
-        if (i >= nr) continue;
-        const double ti = update ? tconst - sh.r[i] * inv_m : 0.0;
+        for (int q = 0; q < NQ; ++q) y[q] = row[32 * q];
+        double racc = 0.0;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          const int j = lane + 32 * q;
-          if (j < nc) {
-            double* yp = &tile[i * p.TCo + j];
-            const double y = *yp;
-            double z = y;
-            if (update) {
-              z = fmax((y + ti) - cj[q], 0.0);                  // P1 then P2 (fp64)
-              dmax = fmax(dmax, fabs(z - y));
-              *yp = z;
-            }
-            racc[u] += z;
-            cacc[q] += z;
-          }
+          double v = (y[q] + ti) - cj[q];                          // P1 (fp64)
+          z[q] = __double2hiint(v) < 0 ? 0.0 : v;                  // P2
+          dq[q] = fmaxf(dq[q], (float)fabs(z[q] - y[q]));
+          racc += z[q];
+          cacc[q] += z[q];
         }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) row[32 * q] = z[q];
+        rowacc[i * 33 + lane] = racc;
       }
+    } else {
+#pragma unroll 2
+      for (int i = warp; i < nr; i += kWarps) {
+        const double* row = &tile[i * kLdt + lane];
+        double racc = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) racc[u] += __shfl_xor_sync(0xffffffffu, racc[u], o);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (i0 + u < nr) {
-            p.rowp[((int64_t)buf * p.PC + pc) * p.m + r0 + i0 + u] = racc[u];
-            tacc += racc[u];
-          }
+        for (int q = 0; q < NQ; ++q) {
+          const double y = row[32 * q];
+          racc += y;
+          cacc[q] += y;
         }
+        rowacc[i * 33 + lane] = racc;
       }
     }
+    float dmax = 0.0f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) dmax = fmaxf(dmax, dq[q]);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) sh.colsum[warp][lane + 32 * q] = cacc[q];
     dmax = warp_max(dmax);
-    if (lane == 0) { sh.red[warp] = tacc; sh.dred[warp] = (float)dmax; }
+    if (lane == 0) sh.dred[warp] = dmax;
     __syncthreads();
+#ifdef FPFP_OC_PROF
+    const long long c1_ = clock64();
+    pc_rows += c1_ - c0_;
+#endif
+    // row partials (own rows) and column partials (own columns), fixed order
+    double rsum = 0.0;
+    for (int t = threadIdx.x; t < nr; t += kThreads) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int l = 0; l < 32; l += 4) {
+        s0 += rowacc[t * 33 + l]; s1 += rowacc[t * 33 + l + 1];
+        s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
+      }
+      const double rs = (s0 + s1) + (s2 + s3);
+      p.rowp[((int64_t)buf * p.PC + pc) * p.m + r0 + t] = rs;
+      rsum += rs;
+    }
     for (int j = threadIdx.x; j < nc; j += kThreads) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
       p.colp[((int64_t)buf * p.PR + pr) * p.m + c0 + j] = s;
     }
+    rsum = warp_sum(rsum);
+    if (lane == 0) sh.red[warp] = rsum;
+    __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
       float d = 0.0f;
@@ -129,6 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       p.tot[buf * nb + b] = t;
       p.dlt[buf * nb + b] = d;
     }
+#ifdef FPFP_OC_PROF
+    pc_cols += clock64() - c1_;
+#endif
   };
 
   // r (own rows), c (own columns), sigma, delta from exchange buffer `buf`, in a fixed order.
@@ -136,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   // sums the PC partials of row t and the PR partials of column t in registers; warp 7 sums the
   // tile totals and deltas. Loads bypass L1 (__ldcg): the buffers are rewritten every other sweep.
   constexpr int kMaxTilesPerLane = 5;   // PR * PC <= 160
-  constexpr int kMaxP = 16;             // PR, PC <= 16
+  constexpr int kMaxP = 12;             // PR, PC <= 12
   auto absorb = [&](int buf, double& sigma, float& delta) {
     const int t = threadIdx.x;
     double rv[kMaxP], cv[kMaxP];
@@ -219,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 
   // write the tile back in fp32 (slack persists across outer iterations, reading A3)
   for (int i = warp; i < nr; i += kWarps)
-    for (int j = lane; j < nc; j += 32) p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] = (float)tile[i * p.TCo + j];
+    for (int j = lane; j < nc; j += 32) p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] = (float)tile[i * kLdt + j];
   if (!p.do_finalize) {
     if (b == 0 && threadIdx.x == 0) {
       p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->delta = (double)delta;
@@ -234,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   double mu_loc = -INFINITY;
   for (int i = warp; i < xr; i += kWarps)
     for (int j = lane; j < xc; j += 32) {
-      const double xt = bb * (double)p.X[(int64_t)(r0 + i) * p.ldX + c0 + j] + a * tile[i * p.TCo + j];
+      const double xt = bb * (double)p.X[(int64_t)(r0 + i) * p.ldX + c0 + j] + a * tile[i * kLdt + j];
       mu_loc = fmax(mu_loc, xt);
     }
   mu_loc = warp_max(mu_loc);
@@ -268,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
     for (int j = lane; j < xc; j += 32) {
       const int64_t o = (int64_t)(r0 + i) * p.ldX + c0 + j;
       const float xo = p.X[o];
-      const double xt = bb * (double)xo + a * tile[i * p.TCo + j];
+      const double xt = bb * (double)xo + a * tile[i * kLdt + j];
       const float xn = (float)(xt / scale);
       rho_loc = fmaxf(rho_loc, (float)fabs((double)xn - (double)xo));
       p.X[o] = xn;
@@ -302,7 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 }  // namespace
 
 static size_t onchip_smem(int TRo, int TCo, int PR, int PC) {
-  return ((size_t)TRo * TCo + (size_t)TRo * PC + (size_t)TCo * PR) * sizeof(double);
+  (void)PR; (void)PC;
+  const size_t ldt = (size_t)round_up(TCo, 32);                      // kLdt of the kernel
+  return ((size_t)TRo * ldt + (size_t)TRo * 33) * sizeof(double);    // tile + lane row partials
 }
 
 using KernFn = void (*)(OnchipArgs);
@@ -326,7 +367,7 @@ bool onchip_fits(int m, int num_sms, int& PR, int& PC, int& TRo, int& TCo) {
   PR = PC = std::max(1, std::min(side, want));
   TRo = (int)ceil_div(m, PR);
   TCo = (int)round_up(ceil_div(m, PC), 4);
-  if (TCo > kOnchipMaxTC || TRo > kOnchipMaxTC || PR * PC > 160 || PR > 16 || PC > 16) return false;
+  if (TCo > kOnchipMaxTC || TRo > kOnchipMaxTC || PR * PC > 160 || PR > 12 || PC > 12) return false;
   const size_t smem = onchip_smem(TRo, TCo, PR, PC);
   if (smem > 190 * 1024) return false;
   // every tile's CTA must be co-resident (cooperative launch); static + dynamic shared memory
