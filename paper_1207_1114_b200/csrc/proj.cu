@@ -39,11 +39,55 @@ struct __align__(16) ProjSmem {
   double bcast[4];
 };
 
+// Row staging for the tile pass (FPFP_PROJ_BULK, default on): every warp owns a ring of kSlots
+// shared-memory row buffers filled by 1-D bulk async copies (cp.async.bulk, the TMA engine) on
+// mbarriers, so kSlots rows per warp (8 KB per CTA per slot depth) are in flight without holding
+// registers; the register-ring path (FPFP_PROJ_BULK=0) keeps kDepth rows of float4 loads instead.
+#ifndef FPFP_PROJ_BULK
+#define FPFP_PROJ_BULK 1
+#endif
+#ifndef FPFP_PROJ_SLOTS
+#define FPFP_PROJ_SLOTS 6
+#endif
+constexpr int kSlots = FPFP_PROJ_SLOTS;
+constexpr size_t kRingBytes = FPFP_PROJ_BULK ? (size_t)kWarps * kSlots * kProjTC * sizeof(float) : 0;
+
+struct Ring {
+  float* buf;          // [kWarps][kSlots][kProjTC] (dynamic shared memory)
+  uint64_t* bar;       // [kWarps][kSlots]
+  uint32_t seq;        // rows consumed by this warp so far (slot = seq % kSlots, parity = seq / kSlots)
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ring_issue(uint64_t* bar, float* dst, const float* src, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 // One tile pass over rows [rb*TR, ...) x cols [cb*512, ...) of Y.
 //   kSweep = false: sums only (Z = Y).   kSweep = true: Z = max(Y + t_i - u_j, 0), written back.
 template <bool kSweep>
 __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double sigma, float& dmax,
-                                          ProjSmem& sm) {
+                                          ProjSmem& sm, Ring& ring_st) {
   const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = rb * p.TR;
@@ -74,9 +118,45 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
     r_hi = ib < row1 ? __ldcg(p.r + ib) : 0.0;
   }
 
-  // Software-pipelined over the warp's rows: a ring of kDepth rows of float4 loads stays in flight
-  // per thread (memory-level parallelism is what bounds this kernel), each slot refilled with the
-  // row kDepth steps ahead as soon as its own row has been corrected and stored.
+  // Software-pipelined over the warp's rows: a ring of kDepth (kSlots) rows stays in flight per
+  // warp (memory-level parallelism is what bounds this kernel), each slot refilled with the row
+  // kDepth steps ahead as soon as its own row has been corrected and stored.
+#if FPFP_PROJ_BULK
+  constexpr int kDepth = kSlots;
+  const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
+  float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
+  uint64_t* wbar = ring_st.bar + warp * kSlots;
+  const uint32_t seq0 = ring_st.seq;
+  const int i0 = row0 + warp;
+  const int nrows_w = i0 < row1 ? (row1 - i0 + kWarps - 1) / kWarps : 0;
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // Y written by the generic proxy
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < kDepth && k < nrows_w; ++k) {
+      const uint32_t slot = (seq0 + k) % kSlots;
+      ring_issue(wbar + slot, wbuf + slot * kProjTC, p.Y + (int64_t)(i0 + k * kWarps) * p.ldY + colbase,
+                 row_bytes);
+    }
+  }
+  __syncwarp();
+  for (int t = 0; t < nrows_w; ++t) {
+    {
+      const int i = i0 + t * kWarps;
+      const uint32_t slot = (seq0 + t) % kSlots;
+      ring_wait(wbar + slot, ((seq0 + t) / kSlots) & 1u);
+      float4 cur[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        cur[q] = inrow[q] ? *reinterpret_cast<const float4*>(wbuf + slot * kProjTC + q * 128 + lane * 4)
+                          : make_float4(0, 0, 0, 0);
+      __syncwarp();
+      if (lane == 0 && t + kDepth < nrows_w) {   // refill this slot with the row kDepth ahead
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        ring_issue(wbar + slot, wbuf + slot * kProjTC,
+                   p.Y + (int64_t)(i + kDepth * kWarps) * p.ldY + colbase, row_bytes);
+      }
+      float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
+#else
   constexpr int kDepth = FPFP_PROJ_DEPTH;
   auto load_row = [&](int i, float4 (&v)[kQ]) {
     const float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
@@ -96,6 +176,7 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
       if (i >= row1) break;
       float4 (&cur)[kQ] = ring[k];
       float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
+#endif
       double ti = 0.0;
       if (kSweep) {
         const int t = (i - row0 - warp) / kWarps;
@@ -131,12 +212,17 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
         for (int q = 0; q < kQ; ++q)
           if (inrow[q]) __stcg(reinterpret_cast<float4*>(rowp + q * 128), cur[q]);
       }
+#if !FPFP_PROJ_BULK
       const int ahead = i + kDepth * kWarps;
       if (ahead < row1) load_row(ahead, ring[k]);
+#endif
       racc = warp_sum(racc);
       if (lane == 0) p.rowpart[(int64_t)cb * p.rows + i] = racc;
     }
   }
+#if FPFP_PROJ_BULK
+  ring_st.seq = seq0 + (uint32_t)nrows_w;
+#endif
   // column partials of this tile: combine the 8 warps in a fixed order
 #pragma unroll
   for (int q = 0; q < kQ; ++q)
@@ -316,12 +402,23 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   if (*p.done) return;  // an earlier iteration of this launch batch converged (uniform)
   cg::grid_group grid = cg::this_grid();
   __shared__ ProjSmem sm;
+  Ring ring{nullptr, nullptr, 0};
+#if FPFP_PROJ_BULK
+  extern __shared__ __align__(128) float ring_smem[];
+  __shared__ __align__(8) uint64_t ring_bar[kWarps * kSlots];
+  ring.buf = ring_smem;
+  ring.bar = ring_bar;
+  if (threadIdx.x < kWarps * kSlots)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&ring_bar[threadIdx.x])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+#endif
   const int ntiles = p.RB * p.CB;
   float dummy = 0.0f;
 
   // ------------------------------------------------------------------ distributed phases
   if (p.mode == kProjSums) {            // sums of the local rows of Y -> c_local, r, sigma_local
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm, ring);
     grid.sync();
     reduce_phase(p, sm);
     grid.sync();
@@ -331,7 +428,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   if (p.mode == kProjOneSweep) {        // one P1+P2 sweep with the global c, sigma = c[m]
     const double sigma = p.c[p.m];
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm, ring);
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
@@ -373,7 +470,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   // ------------------------------------------------------------------ single GPU: everything
   if (p.do_sums) {
     // sums of the current Y (fresh GEMM block + retained slack)
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm, ring);
     grid.sync();
     reduce_phase(p, sm);
     grid.sync();
@@ -384,7 +481,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   float delta = 0.0f;
   for (;;) {
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm, ring);
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
@@ -519,14 +616,20 @@ inline int grid_for(int64_t total) {
 int proj_max_grid(int device) {
   int sms = 0, per_sm = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_kernel, kProjThreads, 0);
+  cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+  cudaFuncSetAttribute(proj_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, proj_kernel, kProjThreads, kRingBytes);
   return sms * std::max(per_sm, 0);
 }
 
 cudaError_t launch_proj(const ProjArgs& a, int grid, cudaStream_t s) {
   ProjArgs copy = a;
   void* args[] = {&copy};
-  return cudaLaunchCooperativeKernel((void*)proj_kernel, dim3(grid), dim3(kProjThreads), args, 0, s);
+  cudaError_t e = cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRingBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(proj_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchCooperativeKernel((void*)proj_kernel, dim3(grid), dim3(kProjThreads), args, kRingBytes, s);
 }
 
 cudaError_t launch_split(const float* src, int64_t lds, float* big, float* small, int64_t ldd,

@@ -26,6 +26,10 @@ namespace {
 #define FPFP_OC_THREADS 256
 #endif
 constexpr int kThreads = FPFP_OC_THREADS;
+#ifndef FPFP_OC_UNROLL
+#define FPFP_OC_UNROLL 2
+#endif
+constexpr int kRowUnroll = FPFP_OC_UNROLL;   // rows of the element loop in flight per warp
 constexpr int kWarps = kThreads / 32;
 
 struct OcShared {
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       cj[q] = j < nc ? sh.c[j] * inv_m : 1e300;
     }
     if (update) {
-#pragma unroll 2
+#pragma unroll kRowUnroll
       for (int i = warp; i < nr; i += kWarps) {
         const double ti = tconst - sh.r[i] * inv_m;
         double* row = &tile[i * kLdt + lane];
@@ -232,9 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.bar), "r"(1u) : "memory");
       const unsigned target = (unsigned)nb * phase;
       unsigned v;
+#ifdef FPFP_OC_RELAXED_POLL
+      // poll without acquire (an acquire load invalidates L1 on every try), then one acquire fence
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
+      } while (v < target);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
       } while (v < target);
+#endif
     }
     __syncthreads();
   };

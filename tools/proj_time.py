@@ -14,4 +14,4 @@ s.iterate(0.5, 0.0, 0, 0, 3, 20, want_x=False)
 st = s.stats()
 ms = st["proj_ms"] / st["proj_launches"]
 byts = 4 * m * m + 8 * m * m * 20 + 28 * m * m
-print(f"{os.environ.get('FASTPFP_LIB','default')}: m={m} proj launch {ms:.3f} ms -> {byts/ms/1e9:.0f} GB/s ; gemm {st['gemm_ms']/st['gemm_launches']:.2f} ms")
+print(f"{os.environ.get('FASTPFP_LIB','default')}: m={m} proj launch {ms:.3f} ms -> {byts/ms/1e6:.0f} GB/s ; gemm {st['gemm_ms']/st['gemm_launches']:.2f} ms")
