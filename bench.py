@@ -149,12 +149,12 @@ def workload_desc(p, workload):
             f"eps1=eps2={p.eps1}, I0=I1={p.max_iter1}")
 
 
-def proj_bytes_per_outer(n, npr, sweeps):
+def proj_bytes_per_outer(n, npr, sweeps, prec=0):
     """Algorithmic HBM bytes of one projection launch: the sums pass reads Y
     (4 m^2), each sweep reads + writes Y (8 m^2), the finalize reads X and Y[0:n,0:n'] twice and
-    writes X and its TF32 split (4 * 7 n n')."""
+    writes X (4 * 5 n n') plus, for the TF32 GEMMs, X's TF32 split (another 4 * 2 n n')."""
     m = max(n, npr)
-    return 4 * m * m + 8 * m * m * sweeps + 28 * n * npr
+    return 4 * m * m + 8 * m * m * sweeps + (20 if prec == 3 else 28) * n * npr
 
 
 def precision_name(prec):
@@ -262,7 +262,7 @@ def run_ours(args):
     peak, bound, peak_note = gemm_peak(mp, src, prec)
     proj_ms = st["proj_ms"] / max(st["proj_launches"], 1)
     rows_local = shard.rows if sharded else p.n
-    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner) * rows_local // p.n
+    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner, prec) * rows_local // p.n
     proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
     step_ms = ms / args.steps
     roofline = {

@@ -862,7 +862,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       pa.Y = h->Y.p; pa.ldY = h->Y.ld; pa.m = (int)h->m;
       pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = N; pa.np = NP;
       pa.alpha = blend; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = max_iter2;
-      pa.rescale = rescale; pa.split = 1; pa.do_finalize = 1; pa.do_sums = 1;
+      // the TF32 split of X feeds only the TF32 GEMMs (the int8 path splits X into digits itself)
+      pa.rescale = rescale; pa.split = h->precision == 3 ? 0 : 1; pa.do_finalize = 1; pa.do_sums = 1;
       pa.TR = h->TR; pa.RB = h->RB; pa.CB = h->CB; pa.RBx = h->RBx; pa.CBx = h->CBx;
       pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c;
       pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;
