@@ -38,13 +38,18 @@ using namespace tc;
 constexpr int kBKb = 128;                 // K bytes (int8 elements) per stage: one 128 B swizzle row
 constexpr int kPRows = 128;               // P rows per CTA
 constexpr int kQRows = 64;                // Q rows per CTA (N = 128 per pair)
-constexpr int kStages = 3;
+#ifndef FPFP_I8_STAGES
+#define FPFP_I8_STAGES 2
+#endif
+constexpr int kStages = FPFP_I8_STAGES;
 constexpr int kPBox = kPRows * kBKb;      // 16 KB
 constexpr int kQBox = kQRows * kBKb;      // 8 KB
 constexpr int kStageBytes = 3 * kPBox + 3 * kQBox;   // 72 KB
 constexpr int kThreads = 256;
 constexpr int kTileM = 256, kTileN = 128;
 constexpr uint32_t kTmemCols = 512;       // 3 x 128 used
+constexpr int kEpiLd = kTileN + 4;        // staged output tile row stride (floats): conflict-free
+constexpr int kEpiBytes = kPRows * kEpiLd * 4;   // 66 KB
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t accumulate) {
@@ -99,6 +104,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
   __shared__ __align__(8) uint64_t tfull_bar;
   __shared__ __align__(8) uint64_t tempty_bar;
   __shared__ uint32_t tmem_base_sm;
+  __shared__ float s_cscale[kTileN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
@@ -190,65 +196,90 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue: TMEM -> registers -> global =====================
+    // ===================== epilogue =====================
+    // E1: TMEM -> registers -> combine -> staged fp32 tile in shared memory (row = TMEM lane), then
+    //     release TMEM so the MMAs of the next tile start at once;
+    // E2: the 4 warps write the staged tile row by row with coalesced float4 stores (adding
+    //     lambda K / the PG term with coalesced loads), overlapping the next tile's main loop.
     const int ew = warp & 3;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = mapa(smem_u32(&tempty_bar), 0);
+    float* stile = reinterpret_cast<float*>(smem + kStages * kStageBytes);   // [128][kEpiLd]
     for (int t = cid; t < num_tiles; t += ncl) {
       int mt, nt;
       tile_coords_i8(t, num_m, num_n, mt, nt);
+      const int rbase = mt * kTileM + (int)rank * kPRows;
+      const int cbase = nt * kTileN;
+      const int lrow = ew * 32 + lane;
+      const int row = rbase + lrow;
+      // column scales 2^(eQ_j - 14) of this tile, staged while the main loop still runs
+      s_cscale[lrow] = cbase + lrow < p.N ? pow2f(__ldg(p.eQ + cbase + lrow) - 14) : 0.0f;
+      const float rscale = row < p.M ? pow2f(p.eP[row]) : 0.0f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(&tfull_bar, acc_phase);
       tc_fence_after();
-      const int row = mt * kTileM + (int)rank * kPRows + ew * 32 + lane;
-      const bool row_ok = row < p.M;
-      const int eP = row_ok ? p.eP[row] : 0;
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16);
       float rmax = 0.0f;
 #pragma unroll 1
       for (int cc = 0; cc < kTileN / 32; ++cc) {
         uint32_t a2[32], a3[32], a4[32];
         __syncwarp();
-        tmem_ld32(tb + (uint32_t)(cc * 32), a2);
-        tmem_ld32(tb + 128u + (uint32_t)(cc * 32), a3);
-        tmem_ld32(tb + 256u + (uint32_t)(cc * 32), a4);
-        if (cc == kTileN / 32 - 1) {   // all accumulator columns are in registers: release TMEM
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader);
-        }
-        const int col0 = nt * kTileN + cc * 32;
-        if (!row_ok || col0 >= p.N) continue;
-        const bool full = col0 + 32 <= p.N;
-        float* c = p.C + (int64_t)row * p.ldC + col0;
-        const float* dd = ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) ? p.D + (int64_t)row * p.ldD + col0 : nullptr;
-        const float* d2 = p.epi == kEpiPG ? p.D2 + (int64_t)row * p.ldD2 + col0 : nullptr;
+        tmem_ld32_nowait(tb + (uint32_t)(cc * 32), a2);
+        tmem_ld32_nowait(tb + 128u + (uint32_t)(cc * 32), a3);
+        tmem_ld32_nowait(tb + 256u + (uint32_t)(cc * 32), a4);
+        tmem_ld_wait();
+        float* srow = stile + lrow * kEpiLd + cc * 32;
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           float o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int col = col0 + j + e;
-            const bool ok = full || col < p.N;
-            const int eQ = ok ? __ldg(p.eQ + col) : 0;
-            // 2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)) * 2^(eP + eQ)
+            // 2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)) * 2^eP * 2^eQ (exact power-of-two scalings)
             float v = fmaf((float)(int)a4[j + e], 0.0078125f, (float)(int)a3[j + e]);
             v = fmaf(v, 0.0078125f, (float)(int)a2[j + e]);
-            v *= pow2f(eP + eQ - 14);
-            if (dd && ok) v += p.lam * dd[j + e];
-            if (d2 && ok) v = p.scale * v + d2[j + e];   // Projected Gradient
+            v = (v * rscale) * s_cscale[cc * 32 + j + e];
             o[e] = v;
-            if (ok) rmax = fmaxf(rmax, fabsf(v));
+            rmax = fmaxf(rmax, fabsf(v));   // columns past N carry scale 0
           }
-          if (full) {
-            *reinterpret_cast<float4*>(c + j) = make_float4(o[0], o[1], o[2], o[3]);
-          } else {
+          *reinterpret_cast<float4*>(srow + j) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader);   // accumulators free
+      if (p.epi == kEpiRowMax && row < p.M) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+      asm volatile("bar.sync 1, 128;" ::: "memory");        // staged tile complete
+      // E2: rows ew, ew + 4, ...: lane l owns columns 4l .. 4l + 3
+      const int col = cbase + lane * 4;
+      const bool cfull = col + 4 <= p.N;
+      for (int r = ew; r < kPRows; r += 4) {
+        const int grow = rbase + r;
+        if (grow >= p.M) break;
+        float4 v = *reinterpret_cast<const float4*>(stile + r * kEpiLd + lane * 4);
+        float* ve = reinterpret_cast<float*>(&v);
+        if (cfull) {
+          if ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) {
+            const float4 dv = *reinterpret_cast<const float4*>(p.D + (int64_t)grow * p.ldD + col);
+            v.x += p.lam * dv.x; v.y += p.lam * dv.y; v.z += p.lam * dv.z; v.w += p.lam * dv.w;
+          }
+          if (p.epi == kEpiPG) {   // Projected Gradient: X + alpha (A X A' + lambda K)
+            const float4 xv = *reinterpret_cast<const float4*>(p.D2 + (int64_t)grow * p.ldD2 + col);
+            v.x = p.scale * v.x + xv.x; v.y = p.scale * v.y + xv.y;
+            v.z = p.scale * v.z + xv.z; v.w = p.scale * v.w + xv.w;
+          }
+          *reinterpret_cast<float4*>(p.C + (int64_t)grow * p.ldC + col) = v;
+        } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (col0 + j + e < p.N) c[j + e] = o[e];
+          for (int e = 0; e < 4; ++e) {
+            if (col + e >= p.N) break;
+            float x = ve[e];
+            if ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) x += p.lam * p.D[(int64_t)grow * p.ldD + col + e];
+            if (p.epi == kEpiPG) x = p.scale * x + p.D2[(int64_t)grow * p.ldD2 + col + e];
+            p.C[(int64_t)grow * p.ldC + col + e] = x;
           }
         }
       }
-      if (p.epi == kEpiRowMax && row_ok) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+      asm volatile("bar.sync 1, 128;" ::: "memory");        // staged tile consumed
       acc_phase ^= 1;
     }
   }
@@ -377,7 +408,7 @@ cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
       return cudaErrorInvalidValue;
   I8Params p{g.M, g.N, g.K, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D, g.ldD, g.lam, g.D2, g.ldD2, g.scale,
              g.rowmax, g.done};
-  const size_t smem = (size_t)kStages * kStageBytes + 1024;
+  const size_t smem = (size_t)kStages * kStageBytes + kEpiBytes + 1024;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
