@@ -87,8 +87,10 @@ typedef enum fastpfp_option {
    * 2 = fp32 SIMT GEMMs (FFMA; the scaffold the tensor-core path is checked against)
    * 3 = Ozaki int8 tensor-core GEMMs (tcgen05 kind::i8; every operand row = a power-of-two scale
    *     and three signed 7-bit digit planes, six exact int32 digit products in three weight
-   *     classes; fp32-accurate). Single-GPU handles only (EUNSUPPORTED when
-   *     sharded); allocates 3 bytes per element of A, A', X, U (+ U in fp32) on first selection. */
+   *     classes; fp32-accurate). Sharded handles need (n/P) % 128 == 0 (else
+   *     EUNSUPPORTED); allocates 3 bytes per element of A, A', X, U (+ U in fp32) on first
+   *     selection. Sharded: the row scales of U are all-reduced (MAX) and U's digit planes, not its
+   *     TF32 parts, are all-gathered (3 instead of 8 bytes per element). */
   FASTPFP_OPT_PRECISION = 2,
   /* 1 (default) = X <- X/max(X) each iteration; 0 = off (Theorem 1 test, reading A11). */
   FASTPFP_OPT_RESCALE = 3,
@@ -196,7 +198,7 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f);
  * GEMM2 Y_r = A_r U^T + lambda K_r with a K-loop over the gathered rank blocks; per sweep an NCCL
  * all-reduce (SUM) of the m column sums and sigma (row sums are local); all-reduce (MAX) of mu
  * and rho. Requirements: n >= n', n % P == 0, (n/P) % 32 == 0 (else
- * EUNSUPPORTED); tensor-core precision (0 or 1).
+ * EUNSUPPORTED); tensor-core precision (0, 1 or 3).
  * On a sharded handle: fastpfp_set_graphs takes the LOCAL rows of A (n/P x n, row-major) and of B
  * (n/P x d) and the full A' and B' (A's symmetry is the caller's contract; finiteness is checked);
  * set_x0 / iterate's X_out / copy_x use the local rows of X (n/P x n'); fastpfp_discretize gathers

@@ -66,7 +66,7 @@ struct fastpfp_handle {
   float* oc_dlt = nullptr;
   unsigned* oc_bar = nullptr;
   // Ozaki int8 operands (FASTPFP_OPT_PRECISION = 3, gemm_i8.cu), allocated on first use
-  I8Buf Ai8, Api8, Xi8, Ui8;
+  I8Buf Ai8, Api8, Xi8, Ui8, Ui8all;   // Ui8all: gathered U digit planes [world][n'][n/P] (sharded)
   unsigned* Urowmax = nullptr;
   bool i8_ready = false;
   // FastGA workspace (ga.cu), allocated on first use of FASTPFP_METHOD_FASTGA
@@ -252,6 +252,7 @@ int i8_prepare(fastpfp_handle* h) {
     CK(h, alloc_i8(h->Api8, (int)h->np, (int)h->np));
     CK(h, alloc_i8(h->Xi8, (int)h->n, (int)h->np));
     CK(h, alloc_i8(h->Ui8, (int)h->np, (int)h->n));
+    if (h->dist) CK(h, alloc_i8(h->Ui8all, (int)(h->world * h->np), (int)h->n));
     CK(h, alloc_arr(h->Urowmax, (size_t)h->np));
     h->i8_ready = true;
   }
@@ -376,7 +377,7 @@ void fastpfp_destroy(fastpfp_handle* h) {
   for (Buf* b : {&h->A, &h->Ab, &h->As, &h->Ap, &h->Apb, &h->Aps, &h->B, &h->Bp, &h->K, &h->X,
                  &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G, &h->Uball, &h->Usall})
     free_buf(*b);
-  for (I8Buf* b : {&h->Ai8, &h->Api8, &h->Xi8, &h->Ui8}) {
+  for (I8Buf* b : {&h->Ai8, &h->Api8, &h->Xi8, &h->Ui8, &h->Ui8all}) {
     for (auto& d : b->d) if (d) cudaFree(d);
     if (b->e) cudaFree(b->e);
   }
@@ -507,7 +508,8 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
     case FASTPFP_OPT_PRECISION:
       if (value < 0 || value > 3) return FASTPFP_EINVAL;
       if (value == 3) {
-        if (h->dist) return set_err(h, FASTPFP_EUNSUPPORTED, "int8 Ozaki GEMM is single-GPU only");
+        if (h->dist && h->n % 128 != 0)
+          return set_err(h, FASTPFP_EUNSUPPORTED, "sharded int8 GEMM needs (n/P) %% 128 == 0");
         h->precision = 3;
         return i8_prepare(h);
       }
@@ -637,6 +639,43 @@ static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo,
                       double pg_alpha = 0.0) {
   cudaStream_t s = h->stream;
   const int N = (int)h->n, NP = (int)h->np;
+  if (h->precision == 3) {
+    // U_r = A' X_r^T (int8 digits, local rows) with its per-row |max| ...
+    CK(h, split_i8(h->X, h->Xi8, nullptr, nullptr, s));
+    I8Gemm g1{};
+    for (int k = 0; k < 3; ++k) { g1.P[k] = h->Api8.d[k]; g1.Q[k] = h->Xi8.d[k]; }
+    g1.ldP = h->Api8.ld; g1.eP = h->Api8.e; g1.ldQ = h->Xi8.ld; g1.eQ = h->Xi8.e;
+    g1.M = NP; g1.N = N; g1.K = NP;
+    g1.epi = kEpiRowMax; g1.C = h->U.p; g1.ldC = h->U.ld; g1.rowmax = h->Urowmax;
+    if (!gemm_i8_supported(g1)) return set_err(h, FASTPFP_EUNSUPPORTED, "int8 GEMM1 unsupported shape");
+    CK(h, cudaMemsetAsync(h->Urowmax, 0, (size_t)NP * sizeof(unsigned), s));
+    CK(h, launch_gemm_i8(g1, s, h->device));
+    // ... the row scales of U are global: MAX over ranks of the |max| bits (nonneg floats order
+    // as unsigned), so every rank splits its block with the same exponents ...
+    NK(h, h->nccl->AllReduce(h->Urowmax, h->Urowmax, (size_t)NP, ncclUint32, ncclMax, h->comm, s));
+    CK(h, split_i8(h->U, h->Ui8, h->Urowmax, nullptr, s));
+    // ... all-gather of the 3 digit planes (3 bytes per element instead of 8 for the TF32 parts)
+    const size_t cnt = (size_t)NP * h->Ui8.ld;
+    NK(h, h->nccl->GroupStart());
+    for (int k = 0; k < 3; ++k)
+      NK(h, h->nccl->AllGather(h->Ui8.d[k], h->Ui8all.d[k], cnt, ncclInt8, h->comm, s));
+    NK(h, h->nccl->GroupEnd());
+    // Y_r[:, 0:n'] = A_r U^T + lambda K_r, K-loop over the gathered rank blocks (3-D TMA)
+    I8Gemm g2{};
+    for (int k = 0; k < 3; ++k) { g2.P[k] = h->Ai8.d[k]; g2.Q[k] = h->Ui8all.d[k]; }
+    g2.ldP = h->Ai8.ld; g2.eP = h->Ai8.e; g2.ldQ = h->Ui8.ld; g2.eQ = h->Ui8.e;
+    g2.M = N; g2.N = NP; g2.K = (int)h->n_glob;
+    g2.q_blocks = h->world; g2.q_block_k = N; g2.q_block_stride = (int64_t)NP * h->Ui8.ld;
+    g2.epi = (add_k && h->method == 1) ? kEpiPG : kEpiAxpy; g2.C = out; g2.ldC = ldo;
+    g2.D = (add_k && lambda != 0.0 && h->d > 0) ? h->K.p : nullptr; g2.ldD = h->K.ld;
+    g2.lam = (float)lambda;
+    g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)pg_alpha;
+    if (!gemm_i8_supported(g2)) return set_err(h, FASTPFP_EUNSUPPORTED, "int8 GEMM2 unsupported shape");
+    CK(h, launch_gemm_i8(g2, s, h->device));
+    h->stats.launches += 4;
+    h->stats.gemm_launches += 2;
+    return FASTPFP_OK;
+  }
   // U_r = A' X_r^T for the local rows r
   GemmArgs g1{};
   g1.P = h->Ap.p; g1.ldP = h->Ap.ld; g1.Pb = h->Apb.p; g1.Ps = h->Aps.p;
@@ -670,7 +709,7 @@ static ProjArgs dist_proj_args(fastpfp_handle* h, int mode, double alpha, double
   pa.X = h->X.p; pa.Xb = h->Xb.p; pa.Xs = h->Xs.p; pa.ldX = h->X.ld; pa.n = (int)h->n;
   pa.np = (int)h->np;
   pa.alpha = alpha; pa.eps1 = eps1; pa.eps2 = eps2; pa.max_iter2 = 1;
-  pa.rescale = h->rescale; pa.split = 1;
+  pa.rescale = h->rescale; pa.split = h->precision == 3 ? 0 : 1;
   pa.TR = h->TR; pa.RB = h->RB; pa.CB = h->CB; pa.RBx = h->RBx; pa.CBx = h->CBx;
   pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c; pa.scal = h->scal;
   pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;

@@ -185,6 +185,9 @@ struct I8Gemm {
   const float* D2; int64_t ldD2; float scale;
   unsigned* rowmax;                 // kEpiRowMax: [M] |max| bits (zeroed by the caller)
   const int* done;
+  // row-sharded GEMM2: Q planes = [q_blocks][N][q_block_k] (block stride in bytes)
+  int q_blocks = 1, q_block_k = 0;
+  int64_t q_block_stride = 0;
 };
 bool gemm_i8_supported(const I8Gemm& g);
 cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device);

@@ -61,6 +61,7 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
 
 struct I8Params {
   int M, N, K;
+  int q3d, qk;                    // Q planes are [K/qk][N][qk] blocks (3-D tensor maps) when q3d
   const int* eP; const int* eQ;   // per-row exponents
   int epi;
   float* C; int64_t ldC;
@@ -150,9 +151,16 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
           tma_load<2>(&mP1, base + 0 * kPBox, bar, kc, prow);
           tma_load<2>(&mP2, base + 1 * kPBox, bar, kc, prow);
           tma_load<2>(&mP3, base + 2 * kPBox, bar, kc, prow);
-          tma_load<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kc, qrow);
-          tma_load<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kc, qrow);
-          tma_load<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kc, qrow);
+          if (p.q3d) {   // row-sharded GEMM2: K walks the gathered rank blocks
+            const int blk = kc / p.qk, kin = kc - blk * p.qk;
+            tma_load3<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kin, qrow, blk);
+            tma_load3<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kin, qrow, blk);
+            tma_load3<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kin, qrow, blk);
+          } else {
+            tma_load<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kc, qrow);
+            tma_load<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kc, qrow);
+            tma_load<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kc, qrow);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -389,6 +397,19 @@ bool make_map_i8(CUtensorMap* m, const int8_t* base, int rows, int K, int64_t ld
   return r == CUDA_SUCCESS;
 }
 
+// [blocks][rows][qk] int8 plane blocks (row stride ld bytes, block stride bstride bytes)
+bool make_map3_i8(CUtensorMap* m, const int8_t* base, int rows, int qk, int blocks, int64_t ld,
+                  int64_t bstride, int box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)qk, (cuuint64_t)rows, (cuuint64_t)blocks};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)bstride};
+  cuuint32_t box[3] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 bool gemm_i8_supported(const I8Gemm& g) {
@@ -397,17 +418,24 @@ bool gemm_i8_supported(const I8Gemm& g) {
   for (int k = 0; k < 3; ++k)
     if (!g.P[k] || !g.Q[k] || (reinterpret_cast<uintptr_t>(g.P[k]) % 16) || (reinterpret_cast<uintptr_t>(g.Q[k]) % 16))
       return false;
+  if (g.q_blocks > 1 && (g.q_block_k % kBKb != 0 || (int64_t)g.q_block_k * g.q_blocks != g.K ||
+                         g.q_block_stride % 16 != 0))
+    return false;
   return (g.ldP % 16 == 0) && (g.ldQ % 16 == 0) && (g.ldC % 4 == 0) && g.eP && g.eQ;
 }
 
 cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
   CUtensorMap mp[3], mq[3];
-  for (int k = 0; k < 3; ++k)
-    if (!make_map_i8(&mp[k], g.P[k], g.M, g.K, g.ldP, kPRows) || !make_map_i8(&mq[k], g.Q[k], g.N, g.K, g.ldQ, kQRows))
-      return cudaErrorInvalidValue;
-  I8Params p{g.M, g.N, g.K, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D, g.ldD, g.lam, g.D2, g.ldD2, g.scale,
-             g.rowmax, g.done};
+  const bool q3d = g.q_blocks > 1;
+  for (int k = 0; k < 3; ++k) {
+    if (!make_map_i8(&mp[k], g.P[k], g.M, g.K, g.ldP, kPRows)) return cudaErrorInvalidValue;
+    const bool ok = q3d ? make_map3_i8(&mq[k], g.Q[k], g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride, kQRows)
+                        : make_map_i8(&mq[k], g.Q[k], g.N, g.K, g.ldQ, kQRows);
+    if (!ok) return cudaErrorInvalidValue;
+  }
+  I8Params p{g.M, g.N, g.K, q3d ? 1 : 0, q3d ? g.q_block_k : 0, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D,
+             g.ldD, g.lam, g.D2, g.ldD2, g.scale, g.rowmax, g.done};
   const size_t smem = (size_t)kStages * kStageBytes + kEpiBytes + 1024;
   static bool attr_set = false;
   if (!attr_set) {

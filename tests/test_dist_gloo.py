@@ -44,7 +44,11 @@ def sharded_outer(sh, A_r, Ap, K_r, X_r, Y_r, lam, alpha, eps2, max_iter2, m):
     """One outer iteration of Algorithm 1 in the sharded decomposition."""
     npr = Ap.shape[0]
     U_r = Ap @ X_r.T                                   # GEMM1, local
+    # int8 path: U's per-row scale must be global (one exponent per row of the gathered U): the
+    # all-reduce MAX of the local row maxima equals the row maxima of the full U
+    rowmax = _allreduce(np.max(np.abs(U_r), axis=1), tdist.ReduceOp.MAX)
     U = _allgather_cols(U_r, sh.world)                 # all-gather of U blocks
+    assert np.array_equal(rowmax, np.max(np.abs(U), axis=1))
     Y_r[:, :npr] = A_r @ U.T + lam * K_r               # GEMM2 (+ lambda K), local rows
     cs = _allreduce(np.append(Y_r.sum(0), Y_r.sum()), tdist.ReduceOp.SUM)
     c, sigma = cs[:m], cs[m]

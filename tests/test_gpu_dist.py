@@ -28,12 +28,15 @@ def _dist_solver(p):
     return F.Solver(p.n, p.n_prime, p.d, dist=(0, 1, uid))
 
 
-def test_dist_world1_matches_single_and_oracle():
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
+def test_dist_world1_matches_single_and_oracle(prec):
     import paper_1207_1114_b200 as F
     p = inputs.config5(n=2048)
     a = F.Solver(p.n, p.n_prime, p.d)
+    a.set_option(F.OPT_PRECISION, prec)
     a.set_graphs(p.A, p.Ap, p.B, p.Bp)
     b = _dist_solver(p)
+    b.set_option(F.OPT_PRECISION, prec)
     b.set_graphs(p.A, p.Ap, p.B, p.Bp)
     st = O.FastPFP(p.A, p.Ap, p.B, p.Bp)
     for t in range(4):
@@ -48,12 +51,14 @@ def test_dist_world1_matches_single_and_oracle():
     assert np.array_equal(b.discretize(), O.greedy_discretize(st.X))
 
 
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
 @pytest.mark.parametrize("slack_mode", [0, 1])
-def test_dist_world1_slack_columns(slack_mode):
+def test_dist_world1_slack_columns(slack_mode, prec):
     import paper_1207_1114_b200 as F
     p = inputs.planted_unequal(77, 1024, 900, d=4, eps1=1e-5, eps2=1e-5, max_iter1=8, max_iter2=60)
     s = _dist_solver(p)
     s.set_option(F.OPT_SLACK_MODE, slack_mode)
+    s.set_option(F.OPT_PRECISION, prec)
     s.set_graphs(p.A, p.Ap, p.B, p.Bp)
     st = O.FastPFP(p.A, p.Ap, p.B, p.Bp, slack_mode="reset" if slack_mode else "persist")
     for t in range(5):
@@ -70,3 +75,7 @@ def test_dist_rejects_unsupported_shapes():
         F.Solver(800, 1000, 0, dist=(0, 1, uid))     # n < n'
     with pytest.raises(F.FastPFPError):
         F.Solver(1000, 1000, 0, dist=(0, 1, uid))    # n/P not a multiple of 32
+    s = F.Solver(96, 96, 0, dist=(0, 1, uid))        # n/P = 96: fine for TF32, not for int8
+    with pytest.raises(F.FastPFPError):
+        s.set_option(F.OPT_PRECISION, F.PREC_INT8_OZAKI)
+    s.close()
