@@ -265,12 +265,21 @@ def run_ours(args):
     pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner, prec) * rows_local // p.n
     proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
     step_ms = ms / args.steps
+    # the same kernel against the tcgen05 issue rate measured on this part (8192 int8 / 2048 TF32
+    # MAC/clk/SM, profiles/r01_tcgen05_peak_micro.txt) at the clock seen during the timed region
+    mac_clk = {3: 8192 / 6.0, 0: 2048 / 3.0, 1: 2048.0}.get(prec)
+    pipe = None
+    if mac_clk and clocks.get("sm_mhz"):
+        pipe_peak = 148 * mac_clk * 2 * clocks["sm_mhz"] * 1e6 / 1e12
+        pipe = {"peak": round(pipe_peak, 1), "frac": round(achieved_tf / pipe_peak, 4),
+                "source": f"measured tcgen05 issue rate x 148 SMs x median SM clock {clocks['sm_mhz']} MHz"}
     roofline = {
         "kernel": f"gemm_{precision_name(prec)}", "bound": bound, "achieved": round(achieved_tf, 2),
         "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
         "traffic": ncu_traffic(f"gemm_{precision_name(prec)}"),
         "flops_per_launch": flops_launch, "ms_per_launch": round(gemm_ms, 4),
         "share_of_step": round(2 * gemm_ms / step_ms, 4), "peak_source": peak_note,
+        "vs_measured_pipe": pipe,
         "note": ("gemm_ms spans both GEMM launches and, when sharded, the NCCL all-gather between them"
                  if sharded else "per GEMM launch (GEMM1 and GEMM2 have equal flops at n = n')"),
         "secondary": {
