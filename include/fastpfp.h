@@ -288,6 +288,14 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
 int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
                     int precision, int cta_group, int64_t stream);
 
+/* The same product with Q re-laid internally as [q_blocks][N][K / q_blocks] — the layout the
+ * row-sharded path's all-gather produces — so the 3-D TMA K-loop of the GEMM2 of a P-rank run is
+ * exercised on one GPU. precision 0, 1 (TF32, (K/q_blocks) % 32 == 0) or 3 (int8 Ozaki,
+ * (K/q_blocks) % 128 == 0; Q's row scales span the whole K as in the sharded run). q_blocks >= 2,
+ * K % q_blocks == 0. Errors: EINVAL, EUNSUPPORTED, ECUDA. */
+int fastpfp_gemm_nt_blocked(const float* P, const float* Q, float* C, int64_t M, int64_t N,
+                            int64_t K, int32_t q_blocks, int precision, int64_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -121,6 +121,7 @@ def lib():
         "fastpfp_batched_destroy": (None, [H]),
         "fastpfp_batched_last_error": (C.c_char_p, [H]),
         "fastpfp_gemm_nt": (C.c_int, [FP, FP, FP, I64, I64, I64, C.c_int, C.c_int, I64]),
+        "fastpfp_gemm_nt_blocked": (C.c_int, [FP, FP, FP, I64, I64, I64, I32, C.c_int, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -319,6 +320,16 @@ def gemm_nt(P, Q, C_out, precision: int = PREC_TF32X3, cta_group: int = 2, strea
     N = Q.shape[0]
     _check(lib().fastpfp_gemm_nt(P.data_ptr(), Q.data_ptr(), C_out.data_ptr(), M, N, K,
                                  int(precision), int(cta_group), int(stream)))
+    return C_out
+
+
+def gemm_nt_blocked(P, Q, C_out, q_blocks: int, precision: int = PREC_TF32X3, stream: int = 0):
+    """C = P Q^T with Q re-laid as [q_blocks][N][K/q_blocks] (fastpfp_gemm_nt_blocked): the
+    row-sharded GEMM2's 3-D TMA K-loop, on one GPU."""
+    M, K = P.shape
+    N = Q.shape[0]
+    _check(lib().fastpfp_gemm_nt_blocked(P.data_ptr(), Q.data_ptr(), C_out.data_ptr(), M, N, K,
+                                         int(q_blocks), int(precision), int(stream)))
     return C_out
 
 

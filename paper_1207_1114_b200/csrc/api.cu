@@ -1136,4 +1136,75 @@ int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t
   return rc;
 }
 
+
+int fastpfp_gemm_nt_blocked(const float* P, const float* Q, float* C, int64_t M, int64_t N,
+                            int64_t K, int32_t q_blocks, int precision, int64_t stream) {
+  // the row-sharded GEMM2 operand layout: Q re-laid as [q_blocks][N][K / q_blocks] (the NCCL
+  // all-gather output), read by the 3-D TMA K-loop of the tensor-core GEMMs
+  if (!P || !Q || !C || M < 1 || N < 1 || K < 1 || q_blocks < 2 || K % q_blocks != 0 ||
+      (precision != 0 && precision != 1 && precision != 3))
+    return FASTPFP_EINVAL;
+  const int64_t kb = K / q_blocks;
+  if (kb % (precision == 3 ? 128 : 32) != 0) return FASTPFP_EUNSUPPORTED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FASTPFP_ENODEV;
+  Buf Pp, Pb, Ps, Qp, Qb, Qs, Cp, Qbb, Qsb;
+  I8Buf Pi, Qi, Qib;
+  int rc = FASTPFP_OK;
+  auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
+  A(alloc_buf(Pp, (int)M, (int)K)); A(alloc_buf(Qp, (int)N, (int)K)); A(alloc_buf(Cp, (int)M, (int)N));
+  if (rc == FASTPFP_OK) {
+    A(upload(Pp, P, 1, s)); A(upload(Qp, Q, 1, s));
+    if (precision == 3) {
+      A(alloc_i8(Pi, (int)M, (int)K)); A(alloc_i8(Qi, (int)N, (int)K));
+      A(alloc_i8(Qib, (int)(q_blocks * N), (int)kb));
+      if (rc == FASTPFP_OK) {
+        A(split_i8(Pp, Pi, nullptr, nullptr, s)); A(split_i8(Qp, Qi, nullptr, nullptr, s));
+        for (int k = 0; k < 3; ++k)
+          for (int b = 0; b < q_blocks; ++b)
+            A(cudaMemcpy2DAsync(Qib.d[k] + (size_t)b * N * Qib.ld, Qib.ld, Qi.d[k] + b * kb, Qi.ld,
+                                kb, N, cudaMemcpyDeviceToDevice, s));
+        I8Gemm gi{};
+        for (int k = 0; k < 3; ++k) { gi.P[k] = Pi.d[k]; gi.Q[k] = Qib.d[k]; }
+        gi.ldP = Pi.ld; gi.eP = Pi.e; gi.ldQ = Qib.ld; gi.eQ = Qi.e;
+        gi.M = (int)M; gi.N = (int)N; gi.K = (int)K; gi.epi = kEpiPlain; gi.C = Cp.p; gi.ldC = Cp.ld;
+        gi.q_blocks = q_blocks; gi.q_block_k = (int)kb; gi.q_block_stride = (int64_t)N * Qib.ld;
+        if (!gemm_i8_supported(gi)) rc = FASTPFP_EUNSUPPORTED;
+        else A(launch_gemm_i8(gi, s, dev));
+      }
+    } else {
+      A(alloc_buf(Pb, (int)M, (int)K)); A(alloc_buf(Ps, (int)M, (int)K));
+      A(alloc_buf(Qb, (int)N, (int)K)); A(alloc_buf(Qs, (int)N, (int)K));
+      A(alloc_buf(Qbb, (int)(q_blocks * N), (int)kb)); A(alloc_buf(Qsb, (int)(q_blocks * N), (int)kb));
+      if (rc == FASTPFP_OK) {
+        A(launch_split(Pp.p, Pp.ld, Pb.p, Ps.p, Pp.ld, (int)M, (int)K, s));
+        A(launch_split(Qp.p, Qp.ld, Qb.p, Qs.p, Qp.ld, (int)N, (int)K, s));
+        for (int b = 0; b < q_blocks; ++b) {
+          A(cudaMemcpy2DAsync(Qbb.p + (size_t)b * N * Qbb.ld, Qbb.ld * 4, Qb.p + b * kb, Qb.ld * 4,
+                              kb * 4, N, cudaMemcpyDeviceToDevice, s));
+          A(cudaMemcpy2DAsync(Qsb.p + (size_t)b * N * Qsb.ld, Qsb.ld * 4, Qs.p + b * kb, Qs.ld * 4,
+                              kb * 4, N, cudaMemcpyDeviceToDevice, s));
+        }
+        GemmArgs g{};
+        g.P = Pp.p; g.ldP = Pp.ld; g.Pb = Pb.p; g.Ps = Ps.p;
+        g.Qb = Qbb.p; g.Qs = Qsb.p; g.ldQ = Qbb.ld;
+        g.M = (int)M; g.N = (int)N; g.K = (int)K; g.epi = kEpiPlain; g.C = Cp.p; g.ldC = Cp.ld;
+        g.cta_group = 2;
+        g.q_blocks = q_blocks; g.q_block_k = (int)kb; g.q_block_stride = (int64_t)N * Qbb.ld;
+        if (!gemm_tc_supported(g)) rc = FASTPFP_EUNSUPPORTED;
+        else A(launch_gemm_tc(g, precision == 1 ? 1 : 3, s, dev));
+      }
+    }
+    if (rc == FASTPFP_OK) A(download(Cp, C, 1, s));
+    A(cudaStreamSynchronize(s));
+  }
+  for (Buf* b : {&Pp, &Pb, &Ps, &Qp, &Qb, &Qs, &Cp, &Qbb, &Qsb}) free_buf(*b);
+  for (I8Buf* b : {&Pi, &Qi, &Qib}) {
+    for (auto& d : b->d) if (d) cudaFree(d);
+    if (b->e) cudaFree(b->e);
+  }
+  return rc;
+}
+
 }  // extern "C"

@@ -35,11 +35,16 @@ namespace {
 
 using namespace tc;
 
-constexpr int kBKb = 128;                 // K bytes (int8 elements) per stage: one 128 B swizzle row
+#ifndef FPFP_I8_KB
+#define FPFP_I8_KB 128
+#endif
+// K bytes (int8 elements) per stage: one swizzle row (128 B -> SWIZZLE_128B, 64 B -> SWIZZLE_64B)
+constexpr int kBKb = FPFP_I8_KB;
+static_assert(kBKb == 128 || kBKb == 64, "K block is one 128- or 64-byte swizzle row");
 constexpr int kPRows = 128;               // P rows per CTA
 constexpr int kQRows = 64;                // Q rows per CTA (N = 128 per pair)
 #ifndef FPFP_I8_STAGES
-#define FPFP_I8_STAGES 2
+#define FPFP_I8_STAGES (FPFP_I8_KB == 128 ? 2 : 4)
 #endif
 constexpr int kStages = FPFP_I8_STAGES;
 constexpr int kPBox = kPRows * kBKb;      // 16 KB
@@ -182,12 +187,13 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
 #pragma unroll
           for (int k = 0; k < kBKb / 32; ++k) {   // K = 32 int8 (32 bytes) per MMA
             const uint32_t off = (uint32_t)k * 32u;
-            const uint64_t p1 = smem_desc(base + 0 * kPBox + off);
-            const uint64_t p2 = smem_desc(base + 1 * kPBox + off);
-            const uint64_t p3 = smem_desc(base + 2 * kPBox + off);
-            const uint64_t q1 = smem_desc(base + 3 * kPBox + 0 * kQBox + off);
-            const uint64_t q2 = smem_desc(base + 3 * kPBox + 1 * kQBox + off);
-            const uint64_t q3 = smem_desc(base + 3 * kPBox + 2 * kQBox + off);
+            auto desc = [](uint32_t a) { return kBKb == 128 ? smem_desc(a) : smem_desc_sw64(a); };
+            const uint64_t p1 = desc(base + 0 * kPBox + off);
+            const uint64_t p2 = desc(base + 1 * kPBox + off);
+            const uint64_t p3 = desc(base + 2 * kPBox + off);
+            const uint64_t q1 = desc(base + 3 * kPBox + 0 * kQBox + off);
+            const uint64_t q2 = desc(base + 3 * kPBox + 1 * kQBox + off);
+            const uint64_t q3 = desc(base + 3 * kPBox + 2 * kQBox + off);
             const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
             mma_i8(acc4, p3, q1, kIdesc, acc);   // weight 2^-28 class first
             mma_i8(acc4, p2, q2, kIdesc, 1u);
@@ -392,7 +398,8 @@ bool make_map_i8(CUtensorMap* m, const int8_t* base, int rows, int K, int64_t ld
   cuuint32_t box[2] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     kBKb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -405,7 +412,8 @@ bool make_map3_i8(CUtensorMap* m, const int8_t* base, int rows, int qk, int bloc
   cuuint32_t box[3] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     kBKb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -116,6 +116,17 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   return d;
 }
 
+// K-major, SWIZZLE_64B descriptor (64-byte rows; 8-row core groups 512 B apart)
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFFu) >> 4);  // start address >> 4            [0,14)
+  d |= (uint64_t)1 << 16;                   // leading byte offset (unused)   [16,30)
+  d |= (uint64_t)(512 >> 4) << 32;          // stride byte offset = 512 B     [32,46)
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm100)     [46,48)
+  d |= (uint64_t)4 << 61;                   // layout: SWIZZLE_64B            [61,64)
+  return d;
+}
+
 // tcgen05.commit: arrive on `bar` (same smem offset in every CTA of `mask`) once all previously
 // issued MMAs of this thread completed.
 template <int CG>

@@ -79,3 +79,25 @@ def test_dist_rejects_unsupported_shapes():
     with pytest.raises(F.FastPFPError):
         s.set_option(F.OPT_PRECISION, F.PREC_INT8_OZAKI)
     s.close()
+
+
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
+@pytest.mark.parametrize("blocks,M,N,kb", [(2, 300, 520, 256), (4, 256, 384, 128), (8, 513, 129, 256)])
+def test_blocked_k_loop_gemm_matches_dense(prec, blocks, M, N, kb):
+    # the 3-D TMA K-loop over [P][N][K/P] rank blocks that GEMM2 of a P-rank run uses (it only runs
+    # when P > 1): same product as the dense GEMM, within the same error bound
+    import paper_1207_1114_b200 as F
+    K = blocks * kb
+    r = np.random.default_rng(blocks * 1000 + M)
+    P = (r.random((M, K)) * (r.random((M, K)) < 0.5)).astype(np.float32)
+    Q = r.random((N, K)).astype(np.float32)
+    Cb = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    Cd = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    F.gemm_nt_blocked(torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda(), Cb, blocks, prec)
+    F.gemm_nt(torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda(), Cd, prec, 2)
+    exact = P.astype(np.float64) @ Q.astype(np.float64).T
+    mag = np.abs(P.astype(np.float64)) @ np.abs(Q.astype(np.float64)).T
+    err_b = np.abs(Cb.cpu().numpy().astype(np.float64) - exact)
+    assert np.all(err_b <= (K * 2.0**-24 + 4 * 2.0**-21) * mag + 1e-30), float(np.max(err_b / (mag + 1e-30)))
+    if prec == 3:   # same digits, same per-class integer sums: identical to the dense int8 product
+        assert np.array_equal(Cb.cpu().numpy(), Cd.cpu().numpy())
