@@ -102,3 +102,18 @@ def test_batched_k_steps_equal_one_call():
     for _ in range(5):
         Xb, _ = b.iterate(0.5, 0.0, 0.0, 0.0, 1, 20)
     assert np.array_equal(Xa, Xb)
+
+
+def test_config4_full_batch_sampled_pairs():
+    # BASELINE configs[3] at full size (8192 pairs of n = 128, the fixed 20 x 20 mode bench.py
+    # times): every pair of the one launch recovers its planted permutation and sampled pairs spread
+    # over the batch (first, last, across CTA waves) match the fp64 oracle within 1e-4
+    probs = inputs.config4(fixed=True)
+    s, X, rep = _solve_batch(probs)
+    assign = s.discretize()
+    assert np.all(rep.iterations == 20) and np.all(rep.sweeps == 400)
+    perms = np.stack([p.perm for p in probs])
+    assert np.mean(np.all(assign == perms, axis=1)) == 1.0
+    for k in (0, 1, 147, 148, 2047, 4096, 6000, 8191):
+        Xo, ro, st = O.solve(probs[k])
+        assert np.max(np.abs(X[k].astype(np.float64) - Xo)) <= 1e-4, k
