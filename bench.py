@@ -494,6 +494,16 @@ def oracle_sample(workload, steps):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
+    if workload == "c4":   # one outer iteration of 64 of the 8192 pairs, scaled to the batch
+        probs = inputs.config4(first=0, count=64)
+        states = [O.FastPFP(q.A, q.Ap) for q in probs]
+        per_step = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            for st in states:
+                st.iterate(0.0, 0.5, 0.0, 0.0, 1, 20)
+            per_step.append((time.perf_counter() - t0) * 8192 / 64)
+        return per_step, cores, f"{steps} oracle outer iteration(s) of 64 c4 pairs (20 sweeps), scaled to 8192 pairs"
     if workload == "c5":
         ns = 4096
         p = inputs.config5(n=ns)
@@ -527,6 +537,71 @@ def cpu_baseline(workload, steps=2):
             "sample": sample, "s_per_outer_scaled": round(t, 3)}
 
 
+def run_c4(args):
+    """--workload c4 (BASELINE configs[3]): 8192 pairs of n = 128 split evenly over the ranks (pair
+    data parallelism, no collective on the path; configs[3] "pairs split evenly over 1/2/4/8 GPUs").
+    A step = one outer iteration (20 sweeps) of every pair; value = pairs * steps / max-over-ranks
+    time (strong scaling of the fixed batch)."""
+    import torch
+
+    import paper_1207_1114_b200 as F
+    from paper_1207_1114_b200 import inputs
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    maybe_init_pg(world, "nccl")
+    batch = 8192
+    per = batch // world
+    first = rank * per
+    count = per if rank < world - 1 else batch - first
+    probs = inputs.config4(batch=batch, first=first, count=count)
+    A, Ap, _, _ = inputs.stack_pairs(probs)
+    s = F.BatchedSolver(count, 128, 128, 0)
+    stream = torch.cuda.current_stream()
+    s.set_option(F.OPT_STREAM, stream.cuda_stream)
+    s.set_graphs(A, Ap)
+    s.iterate(0.5, 0.0, 0.0, 0.0, max(args.warmup, 1), 20, want_x=False)
+    s.set_x0(None)
+    barrier(world)
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _, rep = s.iterate(0.5, 0.0, 0.0, 0.0, args.steps, 20, want_x=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    st = s.stats()
+    # the pair's two n^3 products run on the FP32 pipe (SIMT FFMA): 4 n^3 flop per pair-iteration
+    gflop = 4.0 * 128**3 * batch * args.steps / 1e9
+    achieved = gflop / (ms / 1e3) / 1e3
+    peak = 148 * 128 * 2 * 1.965e9 / 1e12 * world
+    assign = s.discretize()
+    acc = float(np.mean(np.all(assign == np.stack([p.perm for p in probs]), axis=1)))
+    out = {"metric": METRIC, "value": round(batch * args.steps / (ms / 1e3), 1), "unit": "pair_outer_iters/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": "c4 (BASELINE configs[3]): 8192 pairs n=n'=128, ER p=0.3, noise N(0,0.02^2), "
+                                  "lambda=0, 20 sweeps per outer, one pair per CTA, pairs split evenly over ranks",
+                      "parallelism": f"pairs/{world}", "l2": "per-pair working set on chip; inputs 1 GB"},
+           "roofline": {"kernel": "small_solve_kernel", "bound": "alu", "achieved": round(achieved, 2),
+                        "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                        "traffic": None, "note": "GEMM flops only; the 20 on-chip sweeps per outer are latency "
+                                                 "bound (DESIGN.md §8)"},
+           "clocks": clocks, "gpu_launches": int(st["launches"]), "planted_recovery_pairs_rank0": acc}
+    s.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -534,13 +609,15 @@ def run_reference(args):
     per_warm, cores, sample = oracle_sample(args.workload, max(args.warmup, 0)) if args.warmup else ([], 0, "")
     per_step, cores, sample = oracle_sample(args.workload, args.steps)
     total = sum(per_step)
-    value = args.steps / total
-    out = {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    units = 8192 if args.workload == "c4" else 1      # c4: pair-outer-iterations of the batch
+    unit = "pair_outer_iters/s" if args.workload == "c4" else UNIT
+    value = units * args.steps / total
+    out = {"metric": METRIC, "value": round(value, 6), "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": args.workload, "reference": "fp64 numpy oracle (oracle/fastpfp.py) on host cores"},
-           "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
-           "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "cpu_baseline": {"value": round(value, 6), "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": round(value, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
@@ -550,7 +627,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4"])
     ap.add_argument("--precision", type=int, default=int(os.environ.get("FASTPFP_BENCH_PRECISION", "3")))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -560,6 +637,8 @@ def main():
         print("warning: timing rules require >= 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_c4(args)
     else:
         run_ours(args)
 
