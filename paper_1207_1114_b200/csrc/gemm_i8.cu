@@ -56,6 +56,25 @@ constexpr uint32_t kTmemCols = 512;       // 3 x 128 used
 constexpr int kEpiLd = kTileN + 4;        // staged output tile row stride (floats): conflict-free
 constexpr int kEpiBytes = kPRows * kEpiLd * 4;   // 66 KB
 
+// A operand from tensor memory (tcgen05.mma ... [a_tmem], b_desc): the P digit tiles are copied
+// smem -> TMEM once per K step (tcgen05.cp 128x256b, in issue order with the MMAs) and read from
+// there by the three / two / one MMAs that use them, instead of being re-read from shared memory
+// by each of them (the UMMA operand reads plus the TMA fills exceed the 128 B/clk
+// shared-memory bandwidth when A comes from shared memory).
+#ifndef FPFP_I8_ATMEM
+#define FPFP_I8_ATMEM 0
+#endif
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t accumulate) {
   asm volatile(
@@ -150,12 +169,18 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t bar = mapa(smem_u32(&full_bar[stage]), 0);   // the leader's barrier
+#ifdef FPFP_I8_EXP_SKIP_P23   // experiment only: load P plane 1 alone (wrong results; ingress test)
+          if (leader) mbar_expect_tx(&full_bar[stage], (kStageBytes - 2 * kPBox) * 2);
+#else
           if (leader) mbar_expect_tx(&full_bar[stage], kStageBytes * 2);
+#endif
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
           const int kc = kb * kBKb;
           tma_load<2>(&mP1, base + 0 * kPBox, bar, kc, prow);
+#ifndef FPFP_I8_EXP_SKIP_P23
           tma_load<2>(&mP2, base + 1 * kPBox, bar, kc, prow);
           tma_load<2>(&mP3, base + 2 * kPBox, bar, kc, prow);
+#endif
           if (p.q3d) {   // row-sharded GEMM2: K walks the gathered rank blocks
             const int blk = kc / p.qk, kin = kc - blk * p.qk;
             tma_load3<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kin, qrow, blk);
@@ -195,12 +220,26 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
             const uint64_t q2 = desc(base + 3 * kPBox + 1 * kQBox + off);
             const uint64_t q3 = desc(base + 3 * kPBox + 2 * kQBox + off);
             const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
+#if FPFP_I8_ATMEM
+            // P digit tiles -> TMEM columns 384 + 24 b .. (double-buffered by K-step parity)
+            const uint32_t ta = tmem_base + 384u + 24u * (uint32_t)(k & 1);
+            tmem_cp_128x256b(ta + 0u, p1);
+            tmem_cp_128x256b(ta + 8u, p2);
+            tmem_cp_128x256b(ta + 16u, p3);
+            mma_i8_ts(acc4, ta + 16u, q1, kIdesc, acc);   // weight 2^-28 class first
+            mma_i8_ts(acc4, ta + 8u, q2, kIdesc, 1u);
+            mma_i8_ts(acc4, ta + 0u, q3, kIdesc, 1u);
+            mma_i8_ts(acc3, ta + 8u, q1, kIdesc, acc);    // 2^-21
+            mma_i8_ts(acc3, ta + 0u, q2, kIdesc, 1u);
+            mma_i8_ts(acc2, ta + 0u, q1, kIdesc, acc);    // 2^-14
+#else
             mma_i8(acc4, p3, q1, kIdesc, acc);   // weight 2^-28 class first
             mma_i8(acc4, p2, q2, kIdesc, 1u);
             mma_i8(acc4, p1, q3, kIdesc, 1u);
             mma_i8(acc3, p2, q1, kIdesc, acc);   // 2^-21
             mma_i8(acc3, p1, q2, kIdesc, 1u);
             mma_i8(acc2, p1, q1, kIdesc, acc);   // 2^-14
+#endif
           }
           umma_commit<2>(&empty_bar[stage]);     // frees the smem slot in both CTAs
           if (++stage == kStages) { stage = 0; phase ^= 1; }
