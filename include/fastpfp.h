@@ -241,7 +241,7 @@ int fastpfp_device_arch(void);
  * convergence; the same scalars (alpha, lambda, eps, maxIter) apply to all pairs.
  * Arrays are pair-major and dense: A [batch][n][n], A' [batch][n'][n'], B [batch][n][d],
  * B' [batch][n'][d], X [batch][n][n']. Limits: 1 <= n, n' <= 128. Projection arithmetic is fp32
- * here; products are fp32 FFMA. Multi-GPU: pairs are split across ranks by the
+ * here; products are int8 Ozaki tcgen05 MMAs (default) or fp32 FFMA. Multi-GPU: pairs are split across ranks by the
  * caller (one handle per GPU, no communication, BASELINE configs[3] "pairs split evenly").
  * ------------------------------------------------------------------------------------------- */
 typedef struct fastpfp_batched fastpfp_batched;
@@ -265,7 +265,9 @@ int fastpfp_batched_copy_x(fastpfp_batched* h, float* dst, int dst_is_device);
 /* Greedy discretization (ties: smaller row, then column) of every pair on the device:
  * assign [batch][n] (host), assign[p*n + i] = column or -1. */
 int fastpfp_batched_discretize(fastpfp_batched* h, int32_t* assign);
-int fastpfp_batched_set_option(fastpfp_batched* h, int key, int64_t value); /* STREAM, RESCALE */
+/* Options: STREAM, RESCALE, PRECISION (3 = the two products on the int8 tensor cores with the Ozaki
+ * digit decomposition, fp32-accurate, default; 2 = fp32 SIMT FFMA). */
+int fastpfp_batched_set_option(fastpfp_batched* h, int key, int64_t value);
 int fastpfp_batched_get_stats(fastpfp_batched* h, fastpfp_stats* out);
 void fastpfp_batched_destroy(fastpfp_batched* h);
 const char* fastpfp_batched_last_error(const fastpfp_batched* h);

@@ -24,6 +24,7 @@ struct fastpfp_batched {
   cudaStream_t stream = nullptr;
   bool own_stream = false, graphs_set = false, x0_custom = false, poisoned = false;
   int rescale = 1;
+  int precision = 3;   // 3 = int8 Ozaki tensor-core products (small_solve_tc.cu), 2 = SIMT fp32
   fastpfp_stats stats{};
   std::string err;
 };
@@ -196,6 +197,11 @@ int fastpfp_batched_set_option(fastpfp_batched* h, int key, int64_t value) {
     h->rescale = (int)value;
     return FASTPFP_OK;
   }
+  if (key == FASTPFP_OPT_PRECISION) {
+    if (value != 2 && value != 3) return berr(h, FASTPFP_EINVAL, "batched precision: 2 (fp32 SIMT) or 3 (int8 Ozaki)");
+    h->precision = (int)value;
+    return FASTPFP_OK;
+  }
   return berr(h, FASTPFP_EINVAL, "option %d not supported by the batched path", key);
 }
 
@@ -269,7 +275,8 @@ int fastpfp_batched_iterate(fastpfp_batched* h, double alpha, double lambda, dou
   a.max_iter1 = max_iter1; a.max_iter2 = max_iter2; a.rescale = h->rescale;
   a.iters = h->iters; a.conv = h->conv; a.sweeps = h->sweeps; a.rho = h->rho; a.degen = h->degen;
   const int grid = (int)std::min<int64_t>(h->batch, h->num_sms);
-  BCK(h, launch_small_solve(a, grid, h->stream));
+  if (h->precision == 3) BCK(h, launch_small_solve_tc(a, grid, h->stream));
+  else BCK(h, launch_small_solve(a, grid, h->stream));
   h->stats.launches += 1;
   cudaStream_t s = h->stream;
   if (iterations) BCK(h, cudaMemcpyAsync(iterations, h->iters, h->batch * 4, cudaMemcpyDeviceToHost, s));

@@ -20,6 +20,33 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// Ozaki digit helpers (no XU-pipe conversions): round-to-nearest-even via the 1.5 * 2^23 magic
+// constant (exact for |x| < 2^22), exponents from the float bits.
+__device__ __forceinline__ int frexp_exp(float mx) {   // e with mx = f 2^e, f in [0.5, 1); 0 for mx = 0
+  const int bits = __float_as_int(mx);
+  const int E = (bits >> 23) & 0xFF;
+  if (E != 0) return E - 126;
+  int e = 0;
+  if (mx != 0.0f) frexpf(mx, &e);                      // subnormal: rare
+  return e;
+}
+__device__ __forceinline__ float exp2i(int e) {         // exact 2^e
+  return (e > -127 && e < 128) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
+}
+// the three signed 7-bit digits of r0 = x 2^-e (given as x * inv, |r0| < 1), d = clamp(rint(128 r), +-127)
+__device__ __forceinline__ void ozaki_digits3(float x, float inv, int& a, int& b, int& c) {
+  constexpr float kMagic = 12582912.0f;                 // 1.5 * 2^23
+  const float r0 = x * inv * 128.0f;                    // exact (power-of-two scaling)
+  const float fa = fminf(fmaxf((r0 + kMagic) - kMagic, -127.0f), 127.0f);
+  const float r1 = (r0 - fa) * 128.0f;                  // exact remainder
+  const float fb = fminf(fmaxf((r1 + kMagic) - kMagic, -127.0f), 127.0f);
+  const float r2 = (r1 - fb) * 128.0f;
+  const float fc = fminf(fmaxf((r2 + kMagic) - kMagic, -127.0f), 127.0f);
+  a = __float_as_int(fa + kMagic) - 0x4B400000;
+  b = __float_as_int(fb + kMagic) - 0x4B400000;
+  c = __float_as_int(fc + kMagic) - 0x4B400000;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -151,6 +178,9 @@ struct SmallArgs {
 };
 size_t small_smem_bytes();
 cudaError_t launch_small_solve(const SmallArgs& a, int grid, cudaStream_t s);
+// the same whole solve with the products on the int8 tensor cores (small_solve_tc.cu)
+size_t small_tc_smem_bytes();
+cudaError_t launch_small_solve_tc(const SmallArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_small_greedy(const float* X, int batch, int n, int np, int32_t* assign, int grid,
                                 cudaStream_t s);
 

@@ -373,10 +373,9 @@ __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int 
       }
       mx = warp_max(mx);
     }
-    int e = 0;
-    if (mx > 0.0f) frexpf(mx, &e);   // mx = f 2^e, f in [0.5, 1): |x / 2^e| < 1
+    const int e = frexp_exp(mx);     // mx = f 2^e, f in [0.5, 1): |x / 2^e| < 1
     if (lane == 0) ex[r] = e;
-    const float inv = ldexpf(1.0f, -e);
+    const float inv = exp2i(-e);
     int8_t* o1 = d1 + (int64_t)r * ldd;
     int8_t* o2 = d2 + (int64_t)r * ldd;
     int8_t* o3 = d3 + (int64_t)r * ldd;
@@ -394,13 +393,9 @@ __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int 
       int8_t* p3 = reinterpret_cast<int8_t*>(&c3);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        float r0 = v[t] * inv * 128.0f;                       // exact (power-of-two scaling)
-        const float a = fminf(fmaxf(rintf(r0), -127.0f), 127.0f);
-        float r1 = (r0 - a) * 128.0f;                         // exact remainder
-        const float b = fminf(fmaxf(rintf(r1), -127.0f), 127.0f);
-        const float r2 = (r1 - b) * 128.0f;
-        const float c = fminf(fmaxf(rintf(r2), -127.0f), 127.0f);
-        p1[t] = (int8_t)(int)a; p2[t] = (int8_t)(int)b; p3[t] = (int8_t)(int)c;
+        int a, b, c;
+        ozaki_digits3(v[t], inv, a, b, c);
+        p1[t] = (int8_t)a; p2[t] = (int8_t)b; p3[t] = (int8_t)c;
       }
       if (k + 4 <= K) {
         *reinterpret_cast<char4*>(o1 + k) = c1;

@@ -1,0 +1,532 @@
+// small_solve_tc.cu — Algorithm 1 for many small pairs (n, n' <= 128), one pair per
+// CTA, with the two products of line 3 on the int8 tensor cores: the Ozaki digit
+// decomposition of gemm_i8.cu (3 signed 7-bit digit planes per operand row, 6 exact int32 digit
+// products in 3 TMEM accumulators, fp32-accurate) at M = N = K = 128 per CTA
+// (tcgen05.mma.cta_group::1.kind::i8, 24 MMAs per product). BASELINE configs[3] (8192 pairs of 128).
+//
+// Per pair: the digit planes of A and A' are built once in shared memory (swizzled K-major,
+// SWIZZLE_128B: one 128-byte row per matrix row). Per outer iteration:
+//   X (global, L2-resident) -> digits -> GEMM1 U = A' X^T (TMEM) -> U digits (row scales over the
+//   whole row) -> GEMM2 G = A U^T (TMEM) -> + lambda K -> fp32 staging -> Y registers
+//   -> the projection sweeps (same on-chip code as small_solve.cu: Y in registers, fp32 sums)
+//   -> blend + rescale on X in global memory.
+// Replaces the SIMT FFMA products of small_solve.cu, which are bound by shared-memory bandwidth.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace fpfp {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kT = 256;       // threads
+constexpr int kS = 128;       // max n, n', m
+constexpr int kLdG = kS + 4;  // fp32 staging row stride
+constexpr int kPlane = kS * kS;   // one digit plane: 128 rows x 128 bytes
+
+struct __align__(1024) SmemTC {
+  int8_t Pd[3][kPlane];       // A' digit planes (GEMM1 M side)
+  int8_t Ad[3][kPlane];       // A digit planes (GEMM2 M side)
+  int8_t Wd[3][kPlane];       // X digits (GEMM1 N side), then U digits (GEMM2 N side)
+  float G[kS][kLdG];          // GEMM2 output staging (row = TMEM lane)
+  float colp[2][8][kS];       // per-warp column partial sums (double buffered)
+  float dl[2][8];
+  float red[8];
+  int eP[kS], eA[kS], eW[kS]; // row exponents
+  float wmax[2][kS];          // row |max| of U per column half
+  float cscale[kS];           // 2^(e_col - 14) of the N side of the current product
+  uint64_t bar;               // MMA completion
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float pow2(int e) {
+  return (e > -127 && e < 128) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
+}
+
+// byte offset of (row, col) in a SWIZZLE_128B K-major plane (128-byte rows, 1024-byte atoms)
+__device__ __forceinline__ int swz(int row, int col) {
+  return row * 128 + ((((col >> 4) ^ (row & 7))) << 4) + (col & 15);
+}
+
+__device__ __forceinline__ void digits3(float x, float inv, int& a, int& b, int& c) {
+  ozaki_digits3(x, inv, a, b, c);
+}
+__device__ __forceinline__ int pack4(int d0, int d1, int d2, int d3) {
+  return (d0 & 0xFF) | ((d1 & 0xFF) << 8) | ((d2 & 0xFF) << 16) | ((d3 & 0xFF) << 24);
+}
+// 4 consecutive values -> one packed word (4 digits) per plane
+__device__ __forceinline__ void digits4(const float (&v)[4], float inv, int& w1, int& w2, int& w3) {
+  int a[4], b[4], c[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) digits3(v[t], inv, a[t], b[t], c[t]);
+  w1 = pack4(a[0], a[1], a[2], a[3]);
+  w2 = pack4(b[0], b[1], b[2], b[3]);
+  w3 = pack4(c[0], c[1], c[2], c[3]);
+}
+
+// rows x cols fp32 matrix (row-major, ld = cols, rows/cols <= 128) -> 3 swizzled digit planes +
+// row exponents; zero outside. One warp per row (lane l owns columns 4l .. 4l + 3), 4 rows' loads
+// in flight per warp (global/L2 latency bounds this step).
+__device__ __forceinline__ void split_rows_smem(const float* src, int rows, int cols, int8_t (*d)[kPlane],
+                                                int* ex) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = lane * 4;
+  for (int r0 = warp * 4; r0 < kS; r0 += (kT / 32) * 4) {
+    float v[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int r = r0 + u;
+        v[u][t] = (r < rows && c0 + t < cols) ? __ldg(src + (int64_t)r * cols + c0 + t) : 0.0f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u;
+      float mx = fmaxf(fmaxf(fabsf(v[u][0]), fabsf(v[u][1])), fmaxf(fabsf(v[u][2]), fabsf(v[u][3])));
+      mx = warp_max(mx);
+      const int e = frexp_exp(mx);
+      if (lane == 0) ex[r] = e;
+      int w1, w2, w3;
+      digits4(v[u], exp2i(-e), w1, w2, w3);
+      const int o = swz(r, c0);
+      *reinterpret_cast<int*>(&d[0][o]) = w1;
+      *reinterpret_cast<int*>(&d[1][o]) = w2;
+      *reinterpret_cast<int*>(&d[2][o]) = w3;
+    }
+  }
+}
+
+// The digit planes of the new X straight from the Y-tile register layout of the blend (warp w owns
+// rows 16w .. 16w + 15, lane l columns l, l + 32, l + 64, l + 96): no reload from global memory.
+__device__ __forceinline__ void split_tile_smem(const float (&x)[16][4], int8_t (*d)[kPlane], int* ex) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int row = warp * 16 + r;
+    float mx = fmaxf(fmaxf(fabsf(x[r][0]), fabsf(x[r][1])), fmaxf(fabsf(x[r][2]), fabsf(x[r][3])));
+    mx = warp_max(mx);
+    const int e = frexp_exp(mx);
+    if (lane == 0) ex[row] = e;
+    const float inv = exp2i(-e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int a, b, c;
+      digits3(x[r][q], inv, a, b, c);
+      const int o = swz(row, lane + 32 * q);
+      d[0][o] = (int8_t)a; d[1][o] = (int8_t)b; d[2][o] = (int8_t)c;
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_i8_1cta(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// C = P Q^T over K = 128 (zero-padded digits): 4 K steps x 6 digit products into the 3 weight-class
+// accumulators at TMEM columns 0 / 128 / 256. One thread issues, the commit arrives on `bar`.
+__device__ __forceinline__ void issue_product(const int8_t (*P)[kPlane], const int8_t (*Q)[kPlane],
+                                              uint32_t tmem, uint64_t* bar) {
+  constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kS >> 3) << 17) |
+                              ((uint32_t)(kS >> 4) << 24);
+  const uint32_t acc2 = tmem, acc3 = tmem + 128, acc4 = tmem + 256;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t off = (uint32_t)k * 32u;
+    const uint64_t p1 = smem_desc(smem_u32(P[0]) + off), p2 = smem_desc(smem_u32(P[1]) + off),
+                   p3 = smem_desc(smem_u32(P[2]) + off);
+    const uint64_t q1 = smem_desc(smem_u32(Q[0]) + off), q2 = smem_desc(smem_u32(Q[1]) + off),
+                   q3 = smem_desc(smem_u32(Q[2]) + off);
+    const uint32_t acc = k == 0 ? 0u : 1u;
+    mma_i8_1cta(acc4, p3, q1, kIdesc, acc);
+    mma_i8_1cta(acc4, p2, q2, kIdesc, 1u);
+    mma_i8_1cta(acc4, p1, q3, kIdesc, 1u);
+    mma_i8_1cta(acc3, p2, q1, kIdesc, acc);
+    mma_i8_1cta(acc3, p1, q2, kIdesc, 1u);
+    mma_i8_1cta(acc2, p1, q1, kIdesc, acc);
+  }
+  umma_commit<1>(bar);
+}
+
+// This thread's 64 values of row (32 (warp & 3) + lane), columns 64 (warp >> 2) .. + 63, of the
+// digit product, (a2 + 2^-7 (a3 + 2^-7 a4)) * rscale * cscale[col] with cscale = 2^(e_col - 14),
+// written to dst[0..63] (shared memory, fp32); returns their max |value|.
+__device__ __forceinline__ float product_to_smem(uint32_t tmem, float rscale, const float* cscale,
+                                                 float* dst) {
+  const int warp = threadIdx.x >> 5;
+  const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
+  float mx = 0.0f;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    uint32_t a2[32], a3[32], a4[32];
+    tmem_ld32_nowait(tb + (uint32_t)(h * 32), a2);
+    tmem_ld32_nowait(tb + 128u + (uint32_t)(h * 32), a3);
+    tmem_ld32_nowait(tb + 256u + (uint32_t)(h * 32), a4);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int col = (warp >> 2) * 64 + h * 32 + j + t;
+        float v = fmaf((float)(int)a4[j + t], 0.0078125f, (float)(int)a3[j + t]);
+        v = fmaf(v, 0.0078125f, (float)(int)a2[j + t]);
+        o[t] = (v * rscale) * cscale[col];
+        mx = fmaxf(mx, fabsf(o[t]));
+      }
+      *reinterpret_cast<float4*>(dst + h * 32 + j) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  return mx;
+}
+
+// All 32 lanes hold partial sums v[0..15] of 16 rows; on return every lane holds the full sums
+// (the same transpose-butterfly as small_solve.cu).
+__device__ __forceinline__ void rows_allreduce16(float (&v)[16]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float a[8], b4[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float send = hi ? v[k] : v[8 + k], keep = hi ? v[8 + k] : v[k];
+      a[k] = keep + __shfl_xor_sync(F, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? a[k] : a[4 + k], keep = hi ? a[4 + k] : a[k];
+      b4[k] = keep + __shfl_xor_sync(F, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? b4[k] : b4[2 + k], keep = hi ? b4[2 + k] : b4[k];
+      b2[k] = keep + __shfl_xor_sync(F, send, 4);
+    }
+  }
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = keep + __shfl_xor_sync(F, send, 2);
+  }
+  b1 += __shfl_xor_sync(F, b1, 1);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int src = (((r >> 3) & 1) << 4) | (((r >> 2) & 1) << 3) | (((r >> 1) & 1) << 2) | ((r & 1) << 1);
+    v[r] = __shfl_sync(F, b1, src);
+  }
+}
+
+}  // namespace
+
+template <bool kFull, bool kDelta>
+__global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SmemTC& sm = *reinterpret_cast<SmemTC*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = p.n, np = p.np, m = p.m;
+  const float inv_m = 1.0f / (float)m;
+  // epilogue geometry: row = TMEM lane 32 (warp & 3) + lane, columns 64 (warp >> 2) ..
+  const int erow = (warp & 3) * 32 + lane, ecol0 = (warp >> 2) * 64;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  uint32_t bar_phase = 0;
+
+  for (int pair = blockIdx.x; pair < p.batch; pair += gridDim.x) {
+    const float* A = p.A + (int64_t)pair * n * n;
+    const float* Ap = p.Ap + (int64_t)pair * np * np;
+    const float* Kp = p.K ? p.K + (int64_t)pair * n * np : nullptr;
+    float* X = p.X + (int64_t)pair * n * np;
+
+    // digit planes of the constant graphs (A' is GEMM1's M side, A is GEMM2's)
+    split_rows_smem(Ap, np, np, sm.Pd, sm.eP);
+    split_rows_smem(A, n, n, sm.Ad, sm.eA);
+    // Y register tile: rows 16w+r, cols l+32e
+    float y[16][4];
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = warp * 16 + r, j = lane + 32 * e;
+        y[r][e] = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
+      }
+
+    int it = 0, conv = 0, total_sweeps = 0, degen = 0;
+    float rho = 0.f;
+    float xr[16][4];            // X in the Y-tile layout (kept for the blend and the next digits)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = warp * 16 + r, j = lane + 32 * e;
+        xr[r][e] = (i < n && j < np) ? X[(int64_t)i * np + j] : 0.f;
+      }
+    split_tile_smem(xr, sm.Wd, sm.eW);
+#ifdef FPFP_SS_PROF
+    long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define SSP(k) do { const long long t_ = clock64(); tp[k] += t_ - tq; tq = t_; } while (0)
+#else
+#define SSP(k) do { } while (0)
+#endif
+    for (; it < p.max_iter1;) {
+      // ---- U = A' X^T (line 3, first product): X rows (N side) are in Wd / eW
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+        issue_product(sm.Pd, sm.Wd, tmem, &sm.bar);
+      }
+      mbar_wait(&sm.bar, bar_phase);
+      bar_phase ^= 1;
+      tc_fence_after();
+      SSP(0);
+      if (threadIdx.x < kS) sm.cscale[threadIdx.x] = pow2(sm.eW[threadIdx.x] - 14);   // X exps
+      __syncthreads();
+      // U -> fp32 staging rows (row = TMEM lane), then digits with the scale of the whole row
+      const float mx = product_to_smem(tmem, pow2(sm.eP[erow]), sm.cscale, &sm.G[erow][ecol0]);
+      sm.wmax[warp >> 2][erow] = mx;
+      tc_fence_before();
+      __syncthreads();                                     // U staged; X digits / exps consumed
+      {
+        const float rmx = fmaxf(sm.wmax[0][erow], sm.wmax[1][erow]);
+        const int e = frexp_exp(rmx);
+        if (warp < 4) sm.eW[erow] = e;
+        const float inv = exp2i(-e);
+#pragma unroll 4
+        for (int j = 0; j < 64; j += 4) {
+          const float4 g = *reinterpret_cast<const float4*>(&sm.G[erow][ecol0 + j]);
+          const float q[4] = {g.x, g.y, g.z, g.w};
+          int w1, w2, w3;
+          digits4(q, inv, w1, w2, w3);
+          const int o = swz(erow, ecol0 + j);
+          *reinterpret_cast<int*>(&sm.Wd[0][o]) = w1;
+          *reinterpret_cast<int*>(&sm.Wd[1][o]) = w2;
+          *reinterpret_cast<int*>(&sm.Wd[2][o]) = w3;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      SSP(1);
+      // ---- G = A U^T + lambda K (line 3, second product)
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+        issue_product(sm.Ad, sm.Wd, tmem, &sm.bar);
+      }
+      mbar_wait(&sm.bar, bar_phase);
+      bar_phase ^= 1;
+      tc_fence_after();
+      SSP(2);
+      if (threadIdx.x < kS) sm.cscale[threadIdx.x] = pow2(sm.eW[threadIdx.x] - 14);
+      __syncthreads();
+      product_to_smem(tmem, pow2(sm.eA[erow]), sm.cscale, &sm.G[erow][ecol0]);   // G staged
+      if (Kp && erow < n) {                               // + lambda K (line 3)
+        for (int j = 0; j < 64 && ecol0 + j < np; ++j)
+          sm.G[erow][ecol0 + j] += p.lam * Kp[(int64_t)erow * np + ecol0 + j];
+      }
+      tc_fence_before();
+      __syncthreads();
+      // Y[0:n, 0:n'] = G ; slack entries keep their values (reading A3)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = warp * 16 + r;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (i < n && lane + 32 * e < np) y[r][e] = sm.G[i][lane + 32 * e];
+      }
+
+      SSP(3);
+      // ---- projection loop (P1 + P2 per sweep), sums of the current Y first (as small_solve.cu)
+      int buf = 0;
+      float rs[16], cs[4];
+      auto sums = [&](float (&yy)[16][4]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) rs[r] = (yy[r][0] + yy[r][1]) + (yy[r][2] + yy[r][3]);
+        rows_allreduce16(rs);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float s = 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) s += yy[r][e];
+          sm.colp[buf][warp][lane + 32 * e] = s;
+        }
+      };
+      sums(y);
+      float dmax = 0.f;
+      if (lane == 0) sm.dl[buf][warp] = 0.f;
+      __syncthreads();
+      int s = 0;
+      float delta = 0.f;
+      for (;;) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float c = 0.f;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) c += sm.colp[buf][w][lane + 32 * e];
+          cs[e] = c;
+        }
+        const float sigma = warp_sum((cs[0] + cs[1]) + (cs[2] + cs[3]));
+        const float tconst = (1.0f + sigma * inv_m) * inv_m;
+        float cu[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cu[e] = cs[e] * inv_m;
+        buf ^= 1;
+        dmax = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int i = warp * 16 + r;
+          const float ti = tconst - rs[r] * inv_m;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = lane + 32 * e;
+            const float yo = y[r][e];
+            const float z = (kFull || (i < m && j < m)) ? fmaxf((yo + ti) - cu[e], 0.f) : 0.f;  // P1, P2
+            if (kDelta) dmax = fmaxf(dmax, fabsf(z - yo));
+            y[r][e] = z;
+          }
+        }
+        sums(y);
+        if (kDelta) {
+          dmax = warp_max(dmax);
+          if (lane == 0) sm.dl[buf][warp] = dmax;
+        }
+        __syncthreads();
+        delta = 0.f;
+        if (kDelta) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) delta = fmaxf(delta, sm.dl[buf][w]);
+        }
+        ++s;
+        if (delta < p.eps2 || s >= p.max_iter2) break;
+      }
+      total_sweeps += s;
+      SSP(4);
+
+      // ---- blend + rescale (lines 8-9) on X in global memory (coalesced along rows)
+      float xt[16][4];
+      float mu = -INFINITY;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = warp * 16 + r;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = lane + 32 * e;
+          const bool ok = i < n && j < np;
+          const float xo = xr[r][e];
+          xt[r][e] = (1.0f - p.alpha) * xo + p.alpha * y[r][e];
+          if (ok) mu = fmaxf(mu, xt[r][e]);
+        }
+      }
+      mu = warp_max(mu);
+      if (lane == 0) sm.red[warp] = mu;
+      __syncthreads();
+      mu = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) mu = fmaxf(mu, sm.red[w]);
+      __syncthreads();
+      if (!(mu > 1e-30f)) { degen = 1; break; }   // degenerate guard (reading A7), X unchanged
+      const float scale = p.rescale ? mu : 1.0f;
+      float rl = 0.f;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = warp * 16 + r;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = lane + 32 * e;
+          if (i < n && j < np) {
+            const float xn = xt[r][e] / scale;
+            rl = fmaxf(rl, fabsf(xn - xr[r][e]));
+            xr[r][e] = xn;
+          }
+        }
+      }
+      split_tile_smem(xr, sm.Wd, sm.eW);     // digits of the new X for the next GEMM1
+      rl = warp_max(rl);
+      if (lane == 0) sm.red[warp] = rl;
+      __syncthreads();
+      rho = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) rho = fmaxf(rho, sm.red[w]);
+      __syncthreads();
+      ++it;
+      SSP(5);
+      if (rho < p.eps1) { conv = 1; break; }
+    }
+#ifdef FPFP_SS_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0 && pair == 0)
+      printf("ss-prof pair 0: per outer (clk): gemm1 %lld  U-epi+digits %lld  gemm2 %lld  G-epi+stage %lld  sweeps %lld  blend+digits %lld\n",
+             tp[0] / it, tp[1] / it, tp[2] / it, tp[3] / it, tp[4] / it, tp[5] / it);
+#endif
+
+    // write back X (and Y when slack exists)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = warp * 16 + r, j = lane + 32 * e;
+        if (i < n && j < np) X[(int64_t)i * np + j] = xr[r][e];
+      }
+    if (p.Y) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = warp * 16 + r, j = lane + 32 * e;
+          if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = y[r][e];
+        }
+    }
+    if (threadIdx.x == 0) {
+      p.iters[pair] = it; p.conv[pair] = conv; p.sweeps[pair] = total_sweeps;
+      p.rho[pair] = rho; p.degen[pair] = degen;
+    }
+    __syncthreads();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+size_t small_tc_smem_bytes() { return sizeof(SmemTC) + 1024; }
+
+cudaError_t launch_small_solve_tc(const SmallArgs& a, int grid, cudaStream_t s) {
+  const bool full = a.n == kS && a.np == kS;
+  const bool delta = a.eps2 > 0.0f;
+  void (*k)(SmallArgs) = full ? (delta ? small_solve_tc_kernel<true, true> : small_solve_tc_kernel<true, false>)
+                              : (delta ? small_solve_tc_kernel<false, true> : small_solve_tc_kernel<false, false>);
+  const int bytes = (int)small_tc_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kT, bytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fpfp
