@@ -188,6 +188,49 @@ __device__ __forceinline__ float product_to_smem(uint32_t tmem, float rscale, co
   return mx;
 }
 
+// All 32 lanes hold partial maxima v[0..15] of 16 rows; on return every lane holds the row maxima
+// (transpose butterfly as rows_allreduce16: 32 shuffles instead of 16 x 5).
+__device__ __forceinline__ void rows_allmax16(float (&v)[16]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float a[8], b4[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float send = hi ? v[k] : v[8 + k], keep = hi ? v[8 + k] : v[k];
+      a[k] = fmaxf(keep, __shfl_xor_sync(F, send, 16));
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? a[k] : a[4 + k], keep = hi ? a[4 + k] : a[k];
+      b4[k] = fmaxf(keep, __shfl_xor_sync(F, send, 8));
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? b4[k] : b4[2 + k], keep = hi ? b4[2 + k] : b4[k];
+      b2[k] = fmaxf(keep, __shfl_xor_sync(F, send, 4));
+    }
+  }
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = fmaxf(keep, __shfl_xor_sync(F, send, 2));
+  }
+  b1 = fmaxf(b1, __shfl_xor_sync(F, b1, 1));
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int src = (((r >> 3) & 1) << 4) | (((r >> 2) & 1) << 3) | (((r >> 1) & 1) << 2) | ((r & 1) << 1);
+    v[r] = __shfl_sync(F, b1, src);
+  }
+}
+
 // All 32 lanes hold partial sums v[0..15] of 16 rows; on return every lane holds the full sums
 // (the same transpose-butterfly as small_solve.cu).
 __device__ __forceinline__ void rows_allreduce16(float (&v)[16]) {
@@ -427,30 +470,32 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       total_sweeps += s;
       SSP(4);
 
-      // ---- blend + rescale (lines 8-9) on X in global memory (coalesced along rows)
-      float xt[16][4];
-      float mu = -INFINITY;
+      // ---- blend + rescale (lines 8-9) on X (registers), row maxima for the next X digits
+      float xt[16][4], rmx[16];
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const int i = warp * 16 + r;
+        rmx[r] = 0.f;                         // X~ >= 0: 0 is the identity of the max
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int j = lane + 32 * e;
-          const bool ok = i < n && j < np;
-          const float xo = xr[r][e];
-          xt[r][e] = (1.0f - p.alpha) * xo + p.alpha * y[r][e];
-          if (ok) mu = fmaxf(mu, xt[r][e]);
+          xt[r][e] = (1.0f - p.alpha) * xr[r][e] + p.alpha * y[r][e];
+          if (i < n && j < np) rmx[r] = fmaxf(rmx[r], xt[r][e]);
         }
       }
-      mu = warp_max(mu);
+      rows_allmax16(rmx);
+      float mu = rmx[0];
+#pragma unroll
+      for (int r = 1; r < 16; ++r) mu = fmaxf(mu, rmx[r]);
       if (lane == 0) sm.red[warp] = mu;
       __syncthreads();
-      mu = -INFINITY;
+      mu = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) mu = fmaxf(mu, sm.red[w]);
       __syncthreads();
       if (!(mu > 1e-30f)) { degen = 1; break; }   // degenerate guard (reading A7), X unchanged
-      const float scale = p.rescale ? mu : 1.0f;
+      // X / max X as a product with the reciprocal (<= 1 ulp from the quotient)
+      const float inv_scale = p.rescale ? 1.0f / mu : 1.0f;
       float rl = 0.f;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -459,13 +504,31 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         for (int e = 0; e < 4; ++e) {
           const int j = lane + 32 * e;
           if (i < n && j < np) {
-            const float xn = xt[r][e] / scale;
+            const float xn = xt[r][e] * inv_scale;
             rl = fmaxf(rl, fabsf(xn - xr[r][e]));
             xr[r][e] = xn;
           }
         }
       }
-      split_tile_smem(xr, sm.Wd, sm.eW);     // digits of the new X for the next GEMM1
+      SSP(6);
+      // digits of the new X for the next GEMM1; row max of X = (row max of X~) / scale (rounding
+      // and the division are monotonic, so this is the max of the stored values)
+      {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int row = warp * 16 + r;
+          const int e = frexp_exp(rmx[r] * inv_scale);
+          if (lane == 0) sm.eW[row] = e;
+          const float inv = exp2i(-e);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            int a, b, c;
+            digits3(xr[r][q], inv, a, b, c);
+            const int o = swz(row, lane + 32 * q);
+            sm.Wd[0][o] = (int8_t)a; sm.Wd[1][o] = (int8_t)b; sm.Wd[2][o] = (int8_t)c;
+          }
+        }
+      }
       rl = warp_max(rl);
       if (lane == 0) sm.red[warp] = rl;
       __syncthreads();
@@ -479,8 +542,8 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     }
 #ifdef FPFP_SS_PROF
     if (blockIdx.x == 0 && threadIdx.x == 0 && pair == 0)
-      printf("ss-prof pair 0: per outer (clk): gemm1 %lld  U-epi+digits %lld  gemm2 %lld  G-epi+stage %lld  sweeps %lld  blend+digits %lld\n",
-             tp[0] / it, tp[1] / it, tp[2] / it, tp[3] / it, tp[4] / it, tp[5] / it);
+      printf("ss-prof pair 0: per outer (clk): gemm1 %lld  U-epi+digits %lld  gemm2 %lld  G-epi+stage %lld  sweeps %lld  blend %lld  X-digits+rho %lld\n",
+             tp[0] / it, tp[1] / it, tp[2] / it, tp[3] / it, tp[4] / it, tp[6] / it, tp[5] / it);
 #endif
 
     // write back X (and Y when slack exists)
