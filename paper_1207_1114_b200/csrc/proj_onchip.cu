@@ -313,14 +313,14 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
     }
     return;
   }
-  const double scale = p.rescale ? mu : 1.0;
+  const double rcp = p.rescale ? 1.0 / mu : 1.0;   // one reciprocal, a DMUL per element
   float rho_loc = 0.0f;
   for (int i = warp; i < xr; i += kWarps)
     for (int j = lane; j < xc; j += 32) {
       const int64_t o = (int64_t)(r0 + i) * p.ldX + c0 + j;
       const float xo = p.X[o];
       const double xt = bb * (double)xo + a * tile[i * kLdt + j];
-      const float xn = (float)(xt / scale);
+      const float xn = (float)(xt * rcp);
       rho_loc = fmaxf(rho_loc, (float)fabs((double)xn - (double)xo));
       p.X[o] = xn;
       const float hb = tf32_rna(xn);
