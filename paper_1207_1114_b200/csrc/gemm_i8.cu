@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <cstdio>
 
 #include "common.cuh"
 #include "tcgen05.cuh"
@@ -35,45 +36,19 @@ namespace {
 
 using namespace tc;
 
-#ifndef FPFP_I8_KB
-#define FPFP_I8_KB 128
-#endif
-// K bytes (int8 elements) per stage: one swizzle row (128 B -> SWIZZLE_128B, 64 B -> SWIZZLE_64B)
-constexpr int kBKb = FPFP_I8_KB;
-static_assert(kBKb == 128 || kBKb == 64, "K block is one 128- or 64-byte swizzle row");
+constexpr int kBKb = 128;                 // K bytes (int8 elements) per stage: one 128 B swizzle row
 constexpr int kPRows = 128;               // P rows per CTA
-constexpr int kQRows = 64;                // Q rows per CTA (N = 128 per pair)
-#ifndef FPFP_I8_STAGES
-#define FPFP_I8_STAGES (FPFP_I8_KB == 128 ? 2 : 4)
-#endif
-constexpr int kStages = FPFP_I8_STAGES;
-constexpr int kPBox = kPRows * kBKb;      // 16 KB
-constexpr int kQBox = kQRows * kBKb;      // 8 KB
-constexpr int kStageBytes = 3 * kPBox + 3 * kQBox;   // 72 KB
+constexpr int kStages = 2;
+constexpr int kPBox = kPRows * kBKb;      // 16 KB: one P digit plane, this CTA's 128 rows
+constexpr int kFBox = 128 * kBKb;         // 16 KB: a whole Q plane of the tile (N = 128 rows)
+constexpr int kHBox = 64 * kBKb;          // 8 KB: half a Q plane (this CTA's 64 rows)
+// stage: P1 P2 P3 | F (Q1 in the leader CTA, Q2 in the peer) | H3 (Q3 half) | H1 (Q1 half)
+constexpr int kOffF = 3 * kPBox, kOffH3 = kOffF + kFBox, kOffH1 = kOffH3 + kHBox;
+constexpr int kStageBytes = kOffH1 + kHBox;          // 80 KB
 constexpr int kThreads = 256;
 constexpr int kTileM = 256, kTileN = 128;
 constexpr uint32_t kTmemCols = 512;       // 3 x 128 used
-constexpr int kEpiLd = kTileN + 4;        // staged output tile row stride (floats): conflict-free
-constexpr int kEpiBytes = kPRows * kEpiLd * 4;   // 66 KB
-
-// A operand from tensor memory (tcgen05.mma ... [a_tmem], b_desc): the P digit tiles are copied
-// smem -> TMEM once per K step (tcgen05.cp 128x256b, in issue order with the MMAs) and read from
-// there by the three / two / one MMAs that use them, instead of being re-read from shared memory
-// by each of them (the UMMA operand reads plus the TMA fills exceed the 128 B/clk
-// shared-memory bandwidth when A comes from shared memory).
-#ifndef FPFP_I8_ATMEM
-#define FPFP_I8_ATMEM 0
-#endif
-__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
-}
+constexpr int kEpiBytes = kPRows * kTileN * 4;       // 64 KB staged output tile (XOR-swizzled)
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t accumulate) {
@@ -113,14 +88,16 @@ __device__ __forceinline__ float pow2f(int e) {
 
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ CUtensorMap mP2,
-               const __grid_constant__ CUtensorMap mP3, const __grid_constant__ CUtensorMap mQ1,
-               const __grid_constant__ CUtensorMap mQ2, const __grid_constant__ CUtensorMap mQ3,
-               I8Params p) {
+               const __grid_constant__ CUtensorMap mP3, const __grid_constant__ CUtensorMap mQ1f,
+               const __grid_constant__ CUtensorMap mQ2f, const __grid_constant__ CUtensorMap mQ3h,
+               const __grid_constant__ CUtensorMap mQ1h, I8Params p) {
   if (p.done && *p.done) return;  // uniform across the grid
 
-  // D = S32, A = B = signed int8, K-major, N = 128, M = 256 (pair)
+  // D = S32, A = B = signed int8, K-major, M = 256 (pair); N = 128 or 256 (two Q planes side by side)
   constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTileN >> 3) << 17) |
                               ((uint32_t)(kTileM >> 4) << 24);
+  constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(2 * kTileN >> 3) << 17) |
+                               ((uint32_t)(kTileM >> 4) << 24);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -165,31 +142,26 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
         int mt, nt;
         tile_coords_i8(t, num_m, num_n, mt, nt);
         const int prow = mt * kTileM + (int)rank * kPRows;
-        const int qrow = nt * kTileN + (int)rank * kQRows;
+        const int qfull = nt * kTileN, qhalf = nt * kTileN + (int)rank * 64;
+        const CUtensorMap* mF = rank == 0 ? &mQ1f : &mQ2f;   // the merged N = 256 operand [Q1; Q2]
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t bar = mapa(smem_u32(&full_bar[stage]), 0);   // the leader's barrier
-#ifdef FPFP_I8_EXP_SKIP_P23   // experiment only: load P plane 1 alone (wrong results; ingress test)
-          if (leader) mbar_expect_tx(&full_bar[stage], (kStageBytes - 2 * kPBox) * 2);
-#else
           if (leader) mbar_expect_tx(&full_bar[stage], kStageBytes * 2);
-#endif
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
           const int kc = kb * kBKb;
           tma_load<2>(&mP1, base + 0 * kPBox, bar, kc, prow);
-#ifndef FPFP_I8_EXP_SKIP_P23
           tma_load<2>(&mP2, base + 1 * kPBox, bar, kc, prow);
           tma_load<2>(&mP3, base + 2 * kPBox, bar, kc, prow);
-#endif
           if (p.q3d) {   // row-sharded GEMM2: K walks the gathered rank blocks
             const int blk = kc / p.qk, kin = kc - blk * p.qk;
-            tma_load3<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kin, qrow, blk);
-            tma_load3<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kin, qrow, blk);
-            tma_load3<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kin, qrow, blk);
+            tma_load3<2>(mF, base + kOffF, bar, kin, qfull, blk);
+            tma_load3<2>(&mQ3h, base + kOffH3, bar, kin, qhalf, blk);
+            tma_load3<2>(&mQ1h, base + kOffH1, bar, kin, qhalf, blk);
           } else {
-            tma_load<2>(&mQ1, base + 3 * kPBox + 0 * kQBox, bar, kc, qrow);
-            tma_load<2>(&mQ2, base + 3 * kPBox + 1 * kQBox, bar, kc, qrow);
-            tma_load<2>(&mQ3, base + 3 * kPBox + 2 * kQBox, bar, kc, qrow);
+            tma_load<2>(mF, base + kOffF, bar, kc, qfull);
+            tma_load<2>(&mQ3h, base + kOffH3, bar, kc, qhalf);
+            tma_load<2>(&mQ1h, base + kOffH1, bar, kc, qhalf);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -201,52 +173,61 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_phase = 0;
+#ifdef FPFP_I8_PROF
+      long long t_empty = 0, t_full = 0, t_start = clock64();
+      int ntl = 0;
+#endif
       for (int t = cid; t < num_tiles; t += ncl) {
+#ifdef FPFP_I8_PROF
+        long long w0 = clock64();
+#endif
         mbar_wait(&tempty_bar, acc_phase ^ 1);   // epilogue drained the accumulators
+#ifdef FPFP_I8_PROF
+        t_empty += clock64() - w0;
+#endif
         tc_fence_after();
         const uint32_t acc2 = tmem_base, acc3 = tmem_base + 128, acc4 = tmem_base + 256;
         for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef FPFP_I8_PROF
+          long long w1 = clock64();
+#endif
           mbar_wait(&full_bar[stage], phase);
+#ifdef FPFP_I8_PROF
+          t_full += clock64() - w1;
+#endif
           tc_fence_after();
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
 #pragma unroll
           for (int k = 0; k < kBKb / 32; ++k) {   // K = 32 int8 (32 bytes) per MMA
             const uint32_t off = (uint32_t)k * 32u;
-            auto desc = [](uint32_t a) { return kBKb == 128 ? smem_desc(a) : smem_desc_sw64(a); };
-            const uint64_t p1 = desc(base + 0 * kPBox + off);
-            const uint64_t p2 = desc(base + 1 * kPBox + off);
-            const uint64_t p3 = desc(base + 2 * kPBox + off);
-            const uint64_t q1 = desc(base + 3 * kPBox + 0 * kQBox + off);
-            const uint64_t q2 = desc(base + 3 * kPBox + 1 * kQBox + off);
-            const uint64_t q3 = desc(base + 3 * kPBox + 2 * kQBox + off);
+            const uint64_t p1 = smem_desc(base + 0 * kPBox + off);
+            const uint64_t p2 = smem_desc(base + 1 * kPBox + off);
+            const uint64_t p3 = smem_desc(base + 2 * kPBox + off);
+            const uint64_t qF = smem_desc(base + kOffF + off);     // [Q1; Q2], N = 256
+            const uint64_t q3 = smem_desc(base + kOffH3 + off);    // Q3, N = 128
+            const uint64_t q1 = smem_desc(base + kOffH1 + off);    // Q1, N = 128
             const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
-#if FPFP_I8_ATMEM
-            // P digit tiles -> TMEM columns 384 + 24 b .. (double-buffered by K-step parity)
-            const uint32_t ta = tmem_base + 384u + 24u * (uint32_t)(k & 1);
-            tmem_cp_128x256b(ta + 0u, p1);
-            tmem_cp_128x256b(ta + 8u, p2);
-            tmem_cp_128x256b(ta + 16u, p3);
-            mma_i8_ts(acc4, ta + 16u, q1, kIdesc, acc);   // weight 2^-28 class first
-            mma_i8_ts(acc4, ta + 8u, q2, kIdesc, 1u);
-            mma_i8_ts(acc4, ta + 0u, q3, kIdesc, 1u);
-            mma_i8_ts(acc3, ta + 8u, q1, kIdesc, acc);    // 2^-21
-            mma_i8_ts(acc3, ta + 0u, q2, kIdesc, 1u);
-            mma_i8_ts(acc2, ta + 0u, q1, kIdesc, acc);    // 2^-14
-#else
-            mma_i8(acc4, p3, q1, kIdesc, acc);   // weight 2^-28 class first
-            mma_i8(acc4, p2, q2, kIdesc, 1u);
-            mma_i8(acc4, p1, q3, kIdesc, 1u);
-            mma_i8(acc3, p2, q1, kIdesc, acc);   // 2^-21
-            mma_i8(acc3, p1, q2, kIdesc, 1u);
-            mma_i8(acc2, p1, q1, kIdesc, acc);   // 2^-14
-#endif
+            // the six digit products as four MMAs (accumulators acc2 | acc3 | acc4 are adjacent):
+            //   P1 [Q1; Q2] -> acc2 | acc3,  P1 Q3 -> acc4,  P2 [Q1; Q2] -> acc3 | acc4,  P3 Q1 -> acc4
+            mma_i8(acc2, p1, qF, kIdesc2, acc);   // initialises acc2 and acc3
+            mma_i8(acc4, p1, q3, kIdesc, acc);    // initialises acc4
+            mma_i8(acc3, p2, qF, kIdesc2, 1u);
+            mma_i8(acc4, p3, q1, kIdesc, 1u);
           }
           umma_commit<2>(&empty_bar[stage]);     // frees the smem slot in both CTAs
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         umma_commit<2>(&tfull_bar);              // accumulators ready (both CTAs)
         acc_phase ^= 1;
+#ifdef FPFP_I8_PROF
+        ++ntl;
+#endif
       }
+#ifdef FPFP_I8_PROF
+      if (cid == 0 || cid == 37)
+        printf("i8-prof cluster %d: tiles %d total %lld clk, wait-accumulator %lld, wait-operands %lld, issue %lld\n",
+               cid, ntl, clock64() - t_start, t_empty, t_full, clock64() - t_start - t_empty - t_full);
+#endif
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
@@ -257,7 +238,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
     const int ew = warp & 3;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = mapa(smem_u32(&tempty_bar), 0);
-    float* stile = reinterpret_cast<float*>(smem + kStages * kStageBytes);   // [128][kEpiLd]
+    float* stile = reinterpret_cast<float*>(smem + kStages * kStageBytes);   // [128][128], swizzled
     for (int t = cid; t < num_tiles; t += ncl) {
       int mt, nt;
       tile_coords_i8(t, num_m, num_n, mt, nt);
@@ -281,7 +262,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
         tmem_ld32_nowait(tb + 128u + (uint32_t)(cc * 32), a3);
         tmem_ld32_nowait(tb + 256u + (uint32_t)(cc * 32), a4);
         tmem_ld_wait();
-        float* srow = stile + lrow * kEpiLd + cc * 32;
+        float* srow = stile + lrow * kTileN;   // float4 column c stored at (c ^ (row & 31))
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           float o[4];
@@ -294,7 +275,8 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
             o[e] = v;
             rmax = fmaxf(rmax, fabsf(v));   // columns past N carry scale 0
           }
-          *reinterpret_cast<float4*>(srow + j) = make_float4(o[0], o[1], o[2], o[3]);
+          const int c4 = ((cc * 32 + j) >> 2) ^ (lrow & 31);
+          *reinterpret_cast<float4*>(srow + c4 * 4) = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
       tc_fence_before();
@@ -308,7 +290,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
       for (int r = ew; r < kPRows; r += 4) {
         const int grow = rbase + r;
         if (grow >= p.M) break;
-        float4 v = *reinterpret_cast<const float4*>(stile + r * kEpiLd + lane * 4);
+        float4 v = *reinterpret_cast<const float4*>(stile + r * kTileN + ((lane ^ (r & 31)) * 4));
         float* ve = reinterpret_cast<float*>(&v);
         if (cfull) {
           if ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) {
@@ -432,8 +414,7 @@ bool make_map_i8(CUtensorMap* m, const int8_t* base, int rows, int K, int64_t ld
   cuuint32_t box[2] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     kBKb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -446,8 +427,7 @@ bool make_map3_i8(CUtensorMap* m, const int8_t* base, int rows, int qk, int bloc
   cuuint32_t box[3] = {(cuuint32_t)kBKb, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     kBKb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -468,14 +448,19 @@ bool gemm_i8_supported(const I8Gemm& g) {
 
 cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
   if (g.M <= 0 || g.N <= 0) return cudaSuccess;
-  CUtensorMap mp[3], mq[3];
+  CUtensorMap mp[3];
   const bool q3d = g.q_blocks > 1;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 3; ++k)
     if (!make_map_i8(&mp[k], g.P[k], g.M, g.K, g.ldP, kPRows)) return cudaErrorInvalidValue;
-    const bool ok = q3d ? make_map3_i8(&mq[k], g.Q[k], g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride, kQRows)
-                        : make_map_i8(&mq[k], g.Q[k], g.N, g.K, g.ldQ, kQRows);
-    if (!ok) return cudaErrorInvalidValue;
-  }
+  // Q planes: Q1 and Q2 as whole 128-row tile boxes (the merged N = 256 operand), Q3 and Q1 as
+  // 64-row half boxes (the N = 128 operands, split between the CTAs of the pair)
+  CUtensorMap mq1f, mq2f, mq3h, mq1h;
+  auto mk = [&](CUtensorMap* m, const int8_t* base, int box_rows) {
+    return q3d ? make_map3_i8(m, base, g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride, box_rows)
+               : make_map_i8(m, base, g.N, g.K, g.ldQ, box_rows);
+  };
+  if (!mk(&mq1f, g.Q[0], 128) || !mk(&mq2f, g.Q[1], 128) || !mk(&mq3h, g.Q[2], 64) || !mk(&mq1h, g.Q[0], 64))
+    return cudaErrorInvalidValue;
   I8Params p{g.M, g.N, g.K, q3d ? 1 : 0, q3d ? g.q_block_k : 0, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D,
              g.ldD, g.lam, g.D2, g.ldD2, g.scale, g.rowmax, g.done};
   const size_t smem = (size_t)kStages * kStageBytes + kEpiBytes + 1024;
@@ -501,7 +486,7 @@ cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel, mp[0], mp[1], mp[2], mq[0], mq[1], mq[2], p);
+  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel, mp[0], mp[1], mp[2], mq1f, mq2f, mq3h, mq1h, p);
 }
 
 cudaError_t launch_split_i8(const float* src, int64_t lds, int rows, int K, const unsigned* rowmax,
