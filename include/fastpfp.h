@@ -87,7 +87,8 @@ typedef enum fastpfp_option {
    * 2 = fp32 SIMT GEMMs (FFMA; the scaffold the tensor-core path is checked against)
    * 3 = Ozaki int8 tensor-core GEMMs (tcgen05 kind::i8; every operand row = a power-of-two scale
    *     and three signed 7-bit digit planes, six exact int32 digit products in three weight
-   *     classes; fp32-accurate). Sharded handles need (n/P) % 128 == 0 (else
+   *     classes; fp32-accurate). Needs n, n' <= 32768 (exact int32 class sums);
+   *     sharded handles need (n/P) % 128 == 0 (else
    *     EUNSUPPORTED); allocates 3 bytes per element of A, A', X, U (+ U in fp32) on first
    *     selection. Sharded: the row scales of U are all-reduced (MAX) and U's digit planes, not its
    *     TF32 parts, are all-gathered (3 instead of 8 bytes per element). */
@@ -285,7 +286,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
                     double* delta_out, int64_t stream);
 
 /* C[M x N] = P[M x K] * Q[N x K]^T (both operands K-major, i.e. row-major with K contiguous) in
- * the given precision (FASTPFP_OPT_PRECISION values 0-3; 3 needs K <= 131072) and tensor-core tiling cta_group (1 or 2,
+ * the given precision (FASTPFP_OPT_PRECISION values 0-3; 3 needs K <= 32768) and tensor-core tiling cta_group (1 or 2,
  * FASTPFP_OPT_GEMM_CTA_GROUP); the product behind A X A'. */
 int fastpfp_gemm_nt(const float* P, const float* Q, float* C, int64_t M, int64_t N, int64_t K,
                     int precision, int cta_group, int64_t stream);

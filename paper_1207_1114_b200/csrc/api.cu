@@ -508,6 +508,8 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
     case FASTPFP_OPT_PRECISION:
       if (value < 0 || value > 3) return FASTPFP_EINVAL;
       if (value == 3) {
+        if (h->n_glob > 32768 || h->np > 32768)   // exact int32 digit sums need K <= 2^15
+          return set_err(h, FASTPFP_EUNSUPPORTED, "int8 Ozaki GEMM needs n, n' <= 32768");
         if (h->dist && h->n % 128 != 0)
           return set_err(h, FASTPFP_EUNSUPPORTED, "sharded int8 GEMM needs (n/P) %% 128 == 0");
         h->precision = 3;

@@ -7,7 +7,8 @@
 // with e_r = frexp exponent of max_k |x_rk| (so |x / 2^e| < 1) and d_k = clamp(rint(r_k 128), +-127),
 // r_{k+1} = r_k 128 - d_k. The product of two such rows is
 //   sum_k P_ik Q_jk = 2^(eP_i + eQ_j) * sum_{p+q <= 4} 2^-7(p+q) (Dp_i . Dq_j)
-// where every digit dot product is an EXACT int32 (|d| <= 127, K <= 2^17 keeps |sum| < 2^31).
+// where every digit dot product is an EXACT int32: a weight class sums at most 3 digit products of
+// |d| <= 127, so K <= 2^15 keeps |sum| <= 3 * 127^2 * 2^15 < 2^31.
 // The six digit pairs fall into three weight classes w = p + q = 2, 3, 4, accumulated in three
 // int32 TMEM accumulators; the epilogue combines them in fp32 (2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)))
 // and applies the exact power-of-two scales. Dropped pairs (p + q >= 5) and the digit truncation
@@ -436,7 +437,7 @@ bool make_map3_i8(CUtensorMap* m, const int8_t* base, int rows, int qk, int bloc
 
 bool gemm_i8_supported(const I8Gemm& g) {
   if (!get_enc()) return false;
-  if (g.M < 1 || g.N < 1 || g.K < 1 || g.K > (1 << 17)) return false;
+  if (g.M < 1 || g.N < 1 || g.K < 1 || g.K > (1 << 15)) return false;   // int32 class sums
   for (int k = 0; k < 3; ++k)
     if (!g.P[k] || !g.Q[k] || (reinterpret_cast<uintptr_t>(g.P[k]) % 16) || (reinterpret_cast<uintptr_t>(g.Q[k]) % 16))
       return false;
