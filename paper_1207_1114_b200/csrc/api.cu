@@ -743,7 +743,10 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
     pa.mode = kProjOneSweep;
     CK(h, launch_proj(pa, h->grid, s));
     NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
-    NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
+    // the global delta is needed for the inner stop test (eps2 > 0) and for the report of the
+    // last sweep only: with a fixed sweep count the MAX all-reduce runs once, not per sweep
+    if (eps2 > 0.0 || sweeps + 1 >= max_iter2)
+      NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
     h->stats.launches += 1;
     ++sweeps;
     if (sweeps >= max_iter2) break;
