@@ -332,6 +332,23 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
 
 // ---- digit split: one warp per row ----------------------------------------------------------
 // rowmax (nullable): precomputed |max| bits per row (GEMM1's kEpiRowMax); else computed here.
+__device__ __forceinline__ int pack4i(int d0, int d1, int d2, int d3) {
+  return (d0 & 0xFF) | ((d1 & 0xFF) << 8) | ((d2 & 0xFF) << 16) | ((d3 & 0xFF) << 24);
+}
+
+// 4 consecutive values -> one packed word (4 digits) per plane at o[0..2] + k (k % 4 == 0, in range)
+__device__ __forceinline__ void digits_store4(float4 q, float inv, int8_t* o1, int8_t* o2, int8_t* o3, int k) {
+  int a0, b0, c0, a1, b1, c1, a2, b2, c2, a3, b3, c3;
+  ozaki_digits3(q.x, inv, a0, b0, c0);
+  ozaki_digits3(q.y, inv, a1, b1, c1);
+  ozaki_digits3(q.z, inv, a2, b2, c2);
+  ozaki_digits3(q.w, inv, a3, b3, c3);
+  *reinterpret_cast<int*>(o1 + k) = pack4i(a0, a1, a2, a3);
+  *reinterpret_cast<int*>(o2 + k) = pack4i(b0, b1, b2, b3);
+  *reinterpret_cast<int*>(o3 + k) = pack4i(c0, c1, c2, c3);
+}
+
+// one warp per row; 4 float4 loads in flight per lane (HBM-bound at c5: 4 B read + 3 B written)
 __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int rows, int K,
                                 const unsigned* __restrict__ rowmax, int8_t* __restrict__ d1,
                                 int8_t* __restrict__ d2, int8_t* __restrict__ d3, int64_t ldd,
@@ -339,6 +356,7 @@ __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int 
   if (done && *done) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp, nw = gridDim.x * (blockDim.x >> 5);
+  const int Kv = K & ~3;                 // float4-vectorised part
   for (int r = gw; r < rows; r += nw) {
     const float* x = src + (int64_t)r * lds;
     float mx;
@@ -346,14 +364,20 @@ __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int 
       mx = __uint_as_float(rowmax[r]);
     } else {
       mx = 0.0f;
-      for (int k = lane * 4; k < K; k += 128) {
-        if (k + 4 <= K) {
-          const float4 v = *reinterpret_cast<const float4*>(x + k);
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-        } else {
-          for (int e = k; e < K; ++e) mx = fmaxf(mx, fabsf(x[e]));
-        }
+      int k = lane * 4;
+      for (; k + 384 < Kv; k += 512) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(x + k + 128 * u));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
       }
+      for (; k < Kv; k += 128) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + k));
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+      for (int e = Kv + lane; e < K; e += 32) mx = fmaxf(mx, fabsf(x[e]));
       mx = warp_max(mx);
     }
     const int e = frexp_exp(mx);     // mx = f 2^e, f in [0.5, 1): |x / 2^e| < 1
@@ -362,31 +386,19 @@ __global__ void split_i8_kernel(const float* __restrict__ src, int64_t lds, int 
     int8_t* o1 = d1 + (int64_t)r * ldd;
     int8_t* o2 = d2 + (int64_t)r * ldd;
     int8_t* o3 = d3 + (int64_t)r * ldd;
-    for (int k = lane * 4; k < K; k += 128) {
-      float v[4];
-      if (k + 4 <= K) {
-        const float4 q = *reinterpret_cast<const float4*>(x + k);
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-      } else {
-        for (int t = 0; t < 4; ++t) v[t] = k + t < K ? x[k + t] : 0.0f;
-      }
-      char4 c1, c2, c3;
-      int8_t* p1 = reinterpret_cast<int8_t*>(&c1);
-      int8_t* p2 = reinterpret_cast<int8_t*>(&c2);
-      int8_t* p3 = reinterpret_cast<int8_t*>(&c3);
+    int k = lane * 4;
+    for (; k + 384 < Kv; k += 512) {
+      float4 v[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        int a, b, c;
-        ozaki_digits3(v[t], inv, a, b, c);
-        p1[t] = (int8_t)a; p2[t] = (int8_t)b; p3[t] = (int8_t)c;
-      }
-      if (k + 4 <= K) {
-        *reinterpret_cast<char4*>(o1 + k) = c1;
-        *reinterpret_cast<char4*>(o2 + k) = c2;
-        *reinterpret_cast<char4*>(o3 + k) = c3;
-      } else {
-        for (int t = 0; t < 4 && k + t < K; ++t) { o1[k + t] = p1[t]; o2[k + t] = p2[t]; o3[k + t] = p3[t]; }
-      }
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(x + k + 128 * u));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) digits_store4(v[u], inv, o1, o2, o3, k + 128 * u);
+    }
+    for (; k < Kv; k += 128) digits_store4(__ldg(reinterpret_cast<const float4*>(x + k)), inv, o1, o2, o3, k);
+    for (int t = Kv + lane; t < K; t += 32) {
+      int a, b, c;
+      ozaki_digits3(x[t], inv, a, b, c);
+      o1[t] = (int8_t)a; o2[t] = (int8_t)b; o3[t] = (int8_t)c;
     }
   }
 }
