@@ -74,11 +74,12 @@ def _sweeps_agree(g_sw, o_sw, frac=0.9):
     return same >= frac * min(len(g_sw), len(o_sw))
 
 
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
 @pytest.mark.parametrize("shape", [(64, 64), (48, 64), (64, 48), (200, 200), (130, 97)])
-def test_fastga_parity_small(shape):
+def test_fastga_parity_small(shape, prec):
     n, npr = shape
     p = inputs.ga_pair(5, n, npr)
-    diffs, fin, g_it, o_it, g_sw, o_sw, a_g, st = _lockstep(p)
+    diffs, fin, g_it, o_it, g_sw, o_sw, a_g, st = _lockstep(p, prec=prec)
     assert max(diffs) <= X_TOL, diffs
     assert fin <= X_TOL, fin
     assert g_it == o_it, (g_it, o_it)
