@@ -268,23 +268,38 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
 // partials l, l+32, ... and an xor tree combines the lanes (a fixed order => deterministic).
 // Per-block partial of sigma = sum of the c_j this block produced (fixed assignment of j to blocks).
 __device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
+  // one thread per column / row, partials summed in block order (coalesced across threads,
+  // independent loads in flight; fixed order => deterministic)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
-  double local = 0.0;  // meaningful in lane 0
-  for (int j = gw; j < p.m; j += nw) {
-    double s = 0.0;
-#pragma unroll 4
-    for (int rb = lane; rb < p.RB; rb += 32) s += p.colpart[(int64_t)rb * p.m + j];
-    s = warp_sum(s);
-    if (lane == 0) { p.c[j] = s; local += s; }
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  double local = 0.0;
+  for (int j = gt; j < p.m; j += nt) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int rb = 0;
+    for (; rb + 4 <= p.RB; rb += 4) {
+      s0 += __ldcg(p.colpart + (int64_t)(rb + 0) * p.m + j);
+      s1 += __ldcg(p.colpart + (int64_t)(rb + 1) * p.m + j);
+      s2 += __ldcg(p.colpart + (int64_t)(rb + 2) * p.m + j);
+      s3 += __ldcg(p.colpart + (int64_t)(rb + 3) * p.m + j);
+    }
+    for (; rb < p.RB; ++rb) s0 += __ldcg(p.colpart + (int64_t)rb * p.m + j);
+    const double s = (s0 + s1) + (s2 + s3);
+    p.c[j] = s;
+    local += s;
   }
-  for (int i = gw; i < p.rows; i += nw) {
-    double s = 0.0;
-#pragma unroll 4
-    for (int cb = lane; cb < p.CB; cb += 32) s += p.rowpart[(int64_t)cb * p.rows + i];
-    s = warp_sum(s);
-    if (lane == 0) p.r[i] = s;
+  for (int i = gt; i < p.rows; i += nt) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int cb = 0;
+    for (; cb + 4 <= p.CB; cb += 4) {
+      s0 += __ldcg(p.rowpart + (int64_t)(cb + 0) * p.rows + i);
+      s1 += __ldcg(p.rowpart + (int64_t)(cb + 1) * p.rows + i);
+      s2 += __ldcg(p.rowpart + (int64_t)(cb + 2) * p.rows + i);
+      s3 += __ldcg(p.rowpart + (int64_t)(cb + 3) * p.rows + i);
+    }
+    for (; cb < p.CB; ++cb) s0 += __ldcg(p.rowpart + (int64_t)cb * p.rows + i);
+    p.r[i] = (s0 + s1) + (s2 + s3);
   }
+  local = warp_sum(local);
   if (lane == 0) sm.red[warp] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
