@@ -17,10 +17,14 @@
 //
 // Kernel shape: persistent, one CTA pair (cta_group::2) per 256 x 128 output tile; each CTA stages
 // 128 rows of P and 64 rows of Q per 128-byte K block (3 digit planes each, TMA SWIZZLE_128B,
-// 3-stage mbarrier ring, 72 KB per stage); one elected thread issues 6 x 4 UMMAs (K = 32 int8 each)
-// per stage; 3 x 128 TMEM columns hold the accumulators (single-buffered: 384 of 512 columns);
-// 4 epilogue warps read them with tcgen05.ld and apply the fused epilogue. The int8 pipe runs
-// 8192 MAC/clk/SM, 4x the TF32 rate, so 6 int8 MMAs cost half of 3xTF32's three TF32 MMAs.
+// 3-stage mbarrier ring, 72 KB per stage = the whole shared memory); the MMA warp runs its loop
+// warp-uniformly and one elected lane issues 6 x 4 UMMAs (K = 32 int8 each) per stage from uniform
+// registers (a single-lane branch cost an R2UR round trip per MMA: 13% of the GEMM); 3 x 128 TMEM
+// columns hold the accumulators (single-buffered: 384 of 512 columns); 4 epilogue warps read them
+// into registers (one output row per thread), release TMEM at once, and store from registers
+// while the next tile's main loop runs. The int8 pipe runs 8192 MAC/clk/SM, 4x the TF32 rate.
+// Measured at c5 (ncu): tensor pipe 97% active; the SM clock sits at 1.6-1.7 GHz under this load
+// (power), so the GEMM is bound by the tensor pipe at the power-limited clock.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -39,17 +43,15 @@ using namespace tc;
 
 constexpr int kBKb = 128;                 // K bytes (int8 elements) per stage: one 128 B swizzle row
 constexpr int kPRows = 128;               // P rows per CTA
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 constexpr int kPBox = kPRows * kBKb;      // 16 KB: one P digit plane, this CTA's 128 rows
-constexpr int kFBox = 128 * kBKb;         // 16 KB: a whole Q plane of the tile (N = 128 rows)
 constexpr int kHBox = 64 * kBKb;          // 8 KB: half a Q plane (this CTA's 64 rows)
-// stage: P1 P2 P3 | F (Q1 in the leader CTA, Q2 in the peer) | H3 (Q3 half) | H1 (Q1 half)
-constexpr int kOffF = 3 * kPBox, kOffH3 = kOffF + kFBox, kOffH1 = kOffH3 + kHBox;
-constexpr int kStageBytes = kOffH1 + kHBox;          // 80 KB
+// stage: P1 P2 P3 | H1 H2 H3 (this CTA's halves of the three Q planes)
+constexpr int kOffH = 3 * kPBox;
+constexpr int kStageBytes = kOffH + 3 * kHBox;       // 72 KB
 constexpr int kThreads = 256;
 constexpr int kTileM = 256, kTileN = 128;
 constexpr uint32_t kTmemCols = 512;       // 3 x 128 used
-constexpr int kEpiBytes = kPRows * kTileN * 4;       // 64 KB staged output tile (XOR-swizzled)
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                        uint32_t accumulate) {
@@ -89,16 +91,14 @@ __device__ __forceinline__ float pow2f(int e) {
 
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ CUtensorMap mP2,
-               const __grid_constant__ CUtensorMap mP3, const __grid_constant__ CUtensorMap mQ1f,
-               const __grid_constant__ CUtensorMap mQ2f, const __grid_constant__ CUtensorMap mQ3h,
-               const __grid_constant__ CUtensorMap mQ1h, I8Params p) {
+               const __grid_constant__ CUtensorMap mP3, const __grid_constant__ CUtensorMap mQ1,
+               const __grid_constant__ CUtensorMap mQ2, const __grid_constant__ CUtensorMap mQ3,
+               I8Params p) {
   if (p.done && *p.done) return;  // uniform across the grid
 
-  // D = S32, A = B = signed int8, K-major, M = 256 (pair); N = 128 or 256 (two Q planes side by side)
+  // D = S32, A = B = signed int8, K-major, M = 256 (pair), N = 128
   constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTileN >> 3) << 17) |
                               ((uint32_t)(kTileM >> 4) << 24);
-  constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(2 * kTileN >> 3) << 17) |
-                               ((uint32_t)(kTileM >> 4) << 24);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -107,7 +107,7 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
   __shared__ __align__(8) uint64_t tfull_bar;
   __shared__ __align__(8) uint64_t tempty_bar;
   __shared__ uint32_t tmem_base_sm;
-  __shared__ float s_cscale[kTileN];
+  __shared__ float s_cscale[2][kTileN];   // double-buffered by tile parity
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
@@ -143,11 +143,15 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
         int mt, nt;
         tile_coords_i8(t, num_m, num_n, mt, nt);
         const int prow = mt * kTileM + (int)rank * kPRows;
-        const int qfull = nt * kTileN, qhalf = nt * kTileN + (int)rank * 64;
-        const CUtensorMap* mF = rank == 0 ? &mQ1f : &mQ2f;   // the merged N = 256 operand [Q1; Q2]
+        const int qhalf = nt * kTileN + (int)rank * 64;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t bar = mapa(smem_u32(&full_bar[stage]), 0);   // the leader's barrier
+#ifdef FPFP_I8_NOTMA   // experiment: MMA rate alone (operands stale)
+          if (leader) mbar_expect_tx(&full_bar[stage], 0);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          continue;
+#endif
           if (leader) mbar_expect_tx(&full_bar[stage], kStageBytes * 2);
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
           const int kc = kb * kBKb;
@@ -156,13 +160,13 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
           tma_load<2>(&mP3, base + 2 * kPBox, bar, kc, prow);
           if (p.q3d) {   // row-sharded GEMM2: K walks the gathered rank blocks
             const int blk = kc / p.qk, kin = kc - blk * p.qk;
-            tma_load3<2>(mF, base + kOffF, bar, kin, qfull, blk);
-            tma_load3<2>(&mQ3h, base + kOffH3, bar, kin, qhalf, blk);
-            tma_load3<2>(&mQ1h, base + kOffH1, bar, kin, qhalf, blk);
+            tma_load3<2>(&mQ1, base + kOffH + 0 * kHBox, bar, kin, qhalf, blk);
+            tma_load3<2>(&mQ2, base + kOffH + 1 * kHBox, bar, kin, qhalf, blk);
+            tma_load3<2>(&mQ3, base + kOffH + 2 * kHBox, bar, kin, qhalf, blk);
           } else {
-            tma_load<2>(mF, base + kOffF, bar, kc, qfull);
-            tma_load<2>(&mQ3h, base + kOffH3, bar, kc, qhalf);
-            tma_load<2>(&mQ1h, base + kOffH1, bar, kc, qhalf);
+            tma_load<2>(&mQ1, base + kOffH + 0 * kHBox, bar, kc, qhalf);
+            tma_load<2>(&mQ2, base + kOffH + 1 * kHBox, bar, kc, qhalf);
+            tma_load<2>(&mQ3, base + kOffH + 2 * kHBox, bar, kc, qhalf);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -170,12 +174,21 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA, one lane) =====================
-    if (leader && lane == 0) {
+    // the whole warp runs the loop (warp-uniform control flow, descriptors in uniform registers);
+    // one elected lane issues the MMAs and commits
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_phase = 0;
+#ifdef FPFP_I8_CLK
+      const long long c_start = clock64();
+      unsigned long long gc_start;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gc_start));
+#endif
 #ifdef FPFP_I8_PROF
       long long t_empty = 0, t_full = 0, t_start = clock64();
+      unsigned long long g_start;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
       int ntl = 0;
 #endif
       for (int t = cid; t < num_tiles; t += ncl) {
@@ -198,48 +211,67 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
 #endif
           tc_fence_after();
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
+          if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kBKb / 32; ++k) {   // K = 32 int8 (32 bytes) per MMA
             const uint32_t off = (uint32_t)k * 32u;
             const uint64_t p1 = smem_desc(base + 0 * kPBox + off);
             const uint64_t p2 = smem_desc(base + 1 * kPBox + off);
             const uint64_t p3 = smem_desc(base + 2 * kPBox + off);
-            const uint64_t qF = smem_desc(base + kOffF + off);     // [Q1; Q2], N = 256
-            const uint64_t q3 = smem_desc(base + kOffH3 + off);    // Q3, N = 128
-            const uint64_t q1 = smem_desc(base + kOffH1 + off);    // Q1, N = 128
+            const uint64_t q1 = smem_desc(base + kOffH + 0 * kHBox + off);
+            const uint64_t q2 = smem_desc(base + kOffH + 1 * kHBox + off);
+            const uint64_t q3 = smem_desc(base + kOffH + 2 * kHBox + off);
             const uint32_t acc = (kb == 0 && k == 0) ? 0u : 1u;
-            // the six digit products as four MMAs (accumulators acc2 | acc3 | acc4 are adjacent):
-            //   P1 [Q1; Q2] -> acc2 | acc3,  P1 Q3 -> acc4,  P2 [Q1; Q2] -> acc3 | acc4,  P3 Q1 -> acc4
-            mma_i8(acc2, p1, qF, kIdesc2, acc);   // initialises acc2 and acc3
-            mma_i8(acc4, p1, q3, kIdesc, acc);    // initialises acc4
-            mma_i8(acc3, p2, qF, kIdesc2, 1u);
+#ifdef FPFP_I8_NOMMA   // experiment: operand delivery alone
+            if (acc < 2) continue;
+#endif
+            // the six digit products by weight class w = p + q
+            mma_i8(acc2, p1, q1, kIdesc, acc);   // w = 2
+            mma_i8(acc3, p1, q2, kIdesc, acc);   // w = 3
+            mma_i8(acc4, p1, q3, kIdesc, acc);   // w = 4
+            mma_i8(acc3, p2, q1, kIdesc, 1u);
+            mma_i8(acc4, p2, q2, kIdesc, 1u);
             mma_i8(acc4, p3, q1, kIdesc, 1u);
           }
           umma_commit<2>(&empty_bar[stage]);     // frees the smem slot in both CTAs
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit<2>(&tfull_bar);              // accumulators ready (both CTAs)
+        if (elect_one()) umma_commit<2>(&tfull_bar);   // accumulators ready (both CTAs)
+        __syncwarp();
         acc_phase ^= 1;
 #ifdef FPFP_I8_PROF
         ++ntl;
 #endif
       }
+#ifdef FPFP_I8_CLK
+      {
+        unsigned long long gc_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gc_end));
+        const long long c_end = clock64();
+        if (cid == 0 && lane == 0) printf("i8-clk %lld clk in %llu ns (%.0f MHz)\n", c_end - c_start, gc_end - gc_start,
+                             (double)(c_end - c_start) * 1e3 / (double)(gc_end - gc_start));
+      }
+#endif
 #ifdef FPFP_I8_PROF
-      if (cid == 0 || cid == 37)
-        printf("i8-prof cluster %d: tiles %d total %lld clk, wait-accumulator %lld, wait-operands %lld, issue %lld\n",
-               cid, ntl, clock64() - t_start, t_empty, t_full, clock64() - t_start - t_empty - t_full);
+      unsigned long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      if ((cid == 0 || cid == 37) && lane == 0)
+        printf("i8-prof cluster %d: tiles %d total %lld clk in %llu ns (%.0f MHz), wait-accumulator %lld, wait-operands %lld, issue %lld\n",
+               cid, ntl, clock64() - t_start, g_end - g_start, (double)(clock64() - t_start) * 1e3 / (double)(g_end - g_start),
+               t_empty, t_full, clock64() - t_start - t_empty - t_full);
 #endif
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    // E1: TMEM -> registers -> combine -> staged fp32 tile in shared memory (row = TMEM lane), then
-    //     release TMEM so the MMAs of the next tile start at once;
-    // E2: the 4 warps write the staged tile row by row with coalesced float4 stores (adding
-    //     lambda K / the PG term with coalesced loads), overlapping the next tile's main loop.
+    // E1: TMEM -> registers, combined into the 128 fp32 outputs of this thread's row, then TMEM is
+    //     released so the MMAs of the next tile start at once;
+    // E2: the row is written from registers (adding lambda K / the PG term), overlapping the next
+    //     tile's main loop. No shared-memory staging: the whole ring is operand stages.
     const int ew = warp & 3;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = mapa(smem_u32(&tempty_bar), 0);
-    float* stile = reinterpret_cast<float*>(smem + kStages * kStageBytes);   // [128][128], swizzled
     for (int t = cid; t < num_tiles; t += ncl) {
       int mt, nt;
       tile_coords_i8(t, num_m, num_n, mt, nt);
@@ -247,75 +279,69 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
       const int cbase = nt * kTileN;
       const int lrow = ew * 32 + lane;
       const int row = rbase + lrow;
+      float* cs = s_cscale[acc_phase];
       // column scales 2^(eQ_j - 14) of this tile, staged while the main loop still runs
-      s_cscale[lrow] = cbase + lrow < p.N ? pow2f(__ldg(p.eQ + cbase + lrow) - 14) : 0.0f;
+      cs[lrow] = cbase + lrow < p.N ? pow2f(__ldg(p.eQ + cbase + lrow) - 14) : 0.0f;
       const float rscale = row < p.M ? pow2f(p.eP[row]) : 0.0f;
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(&tfull_bar, acc_phase);
+      mbar_wait_sleep(&tfull_bar, acc_phase, 256);   // a whole main loop away: do not spin
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16);
+      float o[kTileN];
       float rmax = 0.0f;
-#pragma unroll 1
-      for (int cc = 0; cc < kTileN / 32; ++cc) {
-        uint32_t a2[32], a3[32], a4[32];
-        __syncwarp();
-        tmem_ld32_nowait(tb + (uint32_t)(cc * 32), a2);
-        tmem_ld32_nowait(tb + 128u + (uint32_t)(cc * 32), a3);
-        tmem_ld32_nowait(tb + 256u + (uint32_t)(cc * 32), a4);
+#pragma unroll
+      for (int cc = 0; cc < kTileN / 16; ++cc) {
+        uint32_t a2[16], a3[16], a4[16];
+        tmem_ld16_nowait(tb + (uint32_t)(cc * 16), a2);
+        tmem_ld16_nowait(tb + 128u + (uint32_t)(cc * 16), a3);
+        tmem_ld16_nowait(tb + 256u + (uint32_t)(cc * 16), a4);
         tmem_ld_wait();
-        float* srow = stile + lrow * kTileN;   // float4 column c stored at (c ^ (row & 31))
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            // 2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)) * 2^eP * 2^eQ (exact power-of-two scalings)
-            float v = fmaf((float)(int)a4[j + e], 0.0078125f, (float)(int)a3[j + e]);
-            v = fmaf(v, 0.0078125f, (float)(int)a2[j + e]);
-            v = (v * rscale) * s_cscale[cc * 32 + j + e];
-            o[e] = v;
-            rmax = fmaxf(rmax, fabsf(v));   // columns past N carry scale 0
-          }
-          const int c4 = ((cc * 32 + j) >> 2) ^ (lrow & 31);
-          *reinterpret_cast<float4*>(srow + c4 * 4) = make_float4(o[0], o[1], o[2], o[3]);
+        for (int j = 0; j < 16; ++j) {
+          // 2^-14 (a2 + 2^-7 (a3 + 2^-7 a4)) * 2^eP * 2^eQ (exact power-of-two scalings)
+          float v = fmaf((float)(int)a4[j], 0.0078125f, (float)(int)a3[j]);
+          v = fmaf(v, 0.0078125f, (float)(int)a2[j]);
+          v = (v * rscale) * cs[cc * 16 + j];
+          o[cc * 16 + j] = v;
+          rmax = fmaxf(rmax, fabsf(v));   // columns past N carry scale 0
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader);   // accumulators free
-      if (p.epi == kEpiRowMax && row < p.M) atomicMax(p.rowmax + row, __float_as_uint(rmax));
-      asm volatile("bar.sync 1, 128;" ::: "memory");        // staged tile complete
-      // E2: rows ew, ew + 4, ...: lane l owns columns 4l .. 4l + 3
-      const int col = cbase + lane * 4;
-      const bool cfull = col + 4 <= p.N;
-      for (int r = ew; r < kPRows; r += 4) {
-        const int grow = rbase + r;
-        if (grow >= p.M) break;
-        float4 v = *reinterpret_cast<const float4*>(stile + r * kTileN + ((lane ^ (r & 31)) * 4));
-        float* ve = reinterpret_cast<float*>(&v);
-        if (cfull) {
-          if ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) {
-            const float4 dv = *reinterpret_cast<const float4*>(p.D + (int64_t)grow * p.ldD + col);
-            v.x += p.lam * dv.x; v.y += p.lam * dv.y; v.z += p.lam * dv.z; v.w += p.lam * dv.w;
+      if (row < p.M) {
+        if (p.epi == kEpiRowMax) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+        float* crow = p.C + (int64_t)row * p.ldC + cbase;
+        const bool add_d = (p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D;
+        const float* drow = add_d ? p.D + (int64_t)row * p.ldD + cbase : nullptr;
+        const float* xrow = p.epi == kEpiPG ? p.D2 + (int64_t)row * p.ldD2 + cbase : nullptr;
+        if (cbase + kTileN <= p.N) {
+#pragma unroll
+          for (int c = 0; c < kTileN; c += 4) {
+            float4 v = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+            if (drow) {
+              const float4 dv = __ldg(reinterpret_cast<const float4*>(drow + c));
+              v.x += p.lam * dv.x; v.y += p.lam * dv.y; v.z += p.lam * dv.z; v.w += p.lam * dv.w;
+            }
+            if (xrow) {   // Projected Gradient: X + alpha (A X A' + lambda K)
+              const float4 xv = __ldg(reinterpret_cast<const float4*>(xrow + c));
+              v.x = p.scale * v.x + xv.x; v.y = p.scale * v.y + xv.y;
+              v.z = p.scale * v.z + xv.z; v.w = p.scale * v.w + xv.w;
+            }
+            *reinterpret_cast<float4*>(crow + c) = v;
           }
-          if (p.epi == kEpiPG) {   // Projected Gradient: X + alpha (A X A' + lambda K)
-            const float4 xv = *reinterpret_cast<const float4*>(p.D2 + (int64_t)grow * p.ldD2 + col);
-            v.x = p.scale * v.x + xv.x; v.y = p.scale * v.y + xv.y;
-            v.z = p.scale * v.z + xv.z; v.w = p.scale * v.w + xv.w;
-          }
-          *reinterpret_cast<float4*>(p.C + (int64_t)grow * p.ldC + col) = v;
         } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (col + e >= p.N) break;
-            float x = ve[e];
-            if ((p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D) x += p.lam * p.D[(int64_t)grow * p.ldD + col + e];
-            if (p.epi == kEpiPG) x = p.scale * x + p.D2[(int64_t)grow * p.ldD2 + col + e];
-            p.C[(int64_t)grow * p.ldC + col + e] = x;
+          for (int c = 0; c < kTileN; ++c) {
+            if (cbase + c < p.N) {
+              float x = o[c];
+              if (drow) x += p.lam * drow[c];
+              if (xrow) x = p.scale * x + xrow[c];
+              crow[c] = x;
+            }
           }
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");        // staged tile consumed
       acc_phase ^= 1;
     }
   }
@@ -465,18 +491,17 @@ cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
   const bool q3d = g.q_blocks > 1;
   for (int k = 0; k < 3; ++k)
     if (!make_map_i8(&mp[k], g.P[k], g.M, g.K, g.ldP, kPRows)) return cudaErrorInvalidValue;
-  // Q planes: Q1 and Q2 as whole 128-row tile boxes (the merged N = 256 operand), Q3 and Q1 as
-  // 64-row half boxes (the N = 128 operands, split between the CTAs of the pair)
-  CUtensorMap mq1f, mq2f, mq3h, mq1h;
+  // Q planes: 64-row half boxes (the N = 128 operands, split between the CTAs of the pair)
+  CUtensorMap mq[3];
   auto mk = [&](CUtensorMap* m, const int8_t* base, int box_rows) {
     return q3d ? make_map3_i8(m, base, g.N, g.q_block_k, g.q_blocks, g.ldQ, g.q_block_stride, box_rows)
                : make_map_i8(m, base, g.N, g.K, g.ldQ, box_rows);
   };
-  if (!mk(&mq1f, g.Q[0], 128) || !mk(&mq2f, g.Q[1], 128) || !mk(&mq3h, g.Q[2], 64) || !mk(&mq1h, g.Q[0], 64))
-    return cudaErrorInvalidValue;
+  for (int k = 0; k < 3; ++k)
+    if (!mk(&mq[k], g.Q[k], 64)) return cudaErrorInvalidValue;
   I8Params p{g.M, g.N, g.K, q3d ? 1 : 0, q3d ? g.q_block_k : 0, g.eP, g.eQ, g.epi, g.C, g.ldC, g.D,
              g.ldD, g.lam, g.D2, g.ldD2, g.scale, g.rowmax, g.done};
-  const size_t smem = (size_t)kStages * kStageBytes + kEpiBytes + 1024;
+  const size_t smem = (size_t)kStages * kStageBytes + 1024;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -499,7 +524,7 @@ cudaError_t launch_gemm_i8(const I8Gemm& g, cudaStream_t s, int device) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel, mp[0], mp[1], mp[2], mq1f, mq2f, mq3h, mq1h, p);
+  return cudaLaunchKernelEx(&cfg, gemm_i8_kernel, mp[0], mp[1], mp[2], mq[0], mq[1], mq[2], p);
 }
 
 cudaError_t launch_split_i8(const float* src, int64_t lds, int rows, int K, const unsigned* rowmax,

@@ -1,0 +1,5 @@
+for i in 1 2; do
+FASTPFP_LIB=varlib/dp.so timeout 300 python tools/prec_time.py c5 3 2>&1 | tail -1
+timeout 300 python tools/prec_time.py c5 3 | tail -1
+FASTPFP_LIB=varlib/clk.so timeout 300 python tools/prec_time.py c5 3 2>&1 | tail -1
+done
