@@ -163,8 +163,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (leader CTA, one lane) =====================
-    if (leader && lane == 0) {
+    // ===================== MMA issuer (leader CTA; warp-uniform loop, one elected lane issues) =====
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -177,6 +177,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t base = smem_u32(smem + stage * kStageBytes);
+          if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {            // K = 8 tf32 (32 bytes) per MMA
             const uint32_t off = (uint32_t)k * 32u;
@@ -194,9 +195,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap mPb, const __grid_constant__ 
             }
           }
           umma_commit<CG>(&empty_bar[stage]);            // frees the smem slot in both CTAs
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit<CG>(&tfull_bar[acc]);                  // accumulator ready (both CTAs)
+        if (elect_one()) umma_commit<CG>(&tfull_bar[acc]);   // accumulator ready (both CTAs)
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }

@@ -341,9 +341,10 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       // ---- U = A' X^T (line 3, first product): X rows (N side) are in Wd / eW
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      if (threadIdx.x == 0) {
+      if (warp == 0) {   // warp-uniform: descriptors stay in uniform registers
         tc_fence_after();
-        issue_product(sm.Pd, sm.Wd, tmem, &sm.bar);
+        if (elect_one()) issue_product(sm.Pd, sm.Wd, tmem, &sm.bar);
+        __syncwarp();
       }
       mbar_wait(&sm.bar, bar_phase);
       bar_phase ^= 1;
@@ -377,9 +378,10 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       __syncthreads();
       SSP(1);
       // ---- G = A U^T + lambda K (line 3, second product)
-      if (threadIdx.x == 0) {
+      if (warp == 0) {   // warp-uniform: descriptors stay in uniform registers
         tc_fence_after();
-        issue_product(sm.Ad, sm.Wd, tmem, &sm.bar);
+        if (elect_one()) issue_product(sm.Ad, sm.Wd, tmem, &sm.bar);
+        __syncwarp();
       }
       mbar_wait(&sm.bar, bar_phase);
       bar_phase ^= 1;
