@@ -200,16 +200,21 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
           const int j = colbase + q * 128 + lane * 4 + e;
           const bool valid = j < p.m;
           const float y = ve[e];
-          float z = y;
+          double zz;
           if (kSweep) {
             const double zd = ((double)y + ti) - u[q][e];          // P1, fp64
-            z = valid ? (float)fmax(zd, 0.0) : 0.0f;                // P2, one rounding to fp32
+#ifdef FPFP_PROJ_SUM_STORED
+            const float z = valid ? (float)fmax(zd, 0.0) : 0.0f;    // P2, one rounding to fp32
+            zz = (double)z;
+#else
+            zz = valid ? fmax(zd, 0.0) : 0.0;                       // P2 in fp64: the sums use it
+            const float z = (float)zz;                              // one rounding to fp32 (stored)
+#endif
             dmax = fmaxf(dmax, fabsf(z - y));                       // delta
             ve[e] = z;
-          } else if (!valid) {
-            z = 0.0f;
+          } else {
+            zz = valid ? (double)y : 0.0;
           }
-          const double zz = (double)z;
           racc += zz;
           colacc[q][e] += zz;
         }

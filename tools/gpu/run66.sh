@@ -1,0 +1,3 @@
+timeout 300 python tools/proj_time.py
+for i in 1 2; do timeout 300 python tools/prec_time.py c5 3 | tail -1; done
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
