@@ -259,14 +259,33 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   absorb(buf, sigma, delta);
 
   int sweeps = 0;
+#ifdef FPFP_OC_PROF
+  long long pc_bar = 0, pc_abs = 0;
+  pc_rows = pc_cols = 0;
+#endif
   for (;;) {
     buf ^= 1;
     pass(true, buf, (1.0 + sigma * inv_m) * inv_m);
+#ifdef FPFP_OC_PROF
+    const long long b0_ = clock64();
+#endif
     exchange_barrier();
+#ifdef FPFP_OC_PROF
+    const long long b1_ = clock64();
+    pc_bar += b1_ - b0_;
+#endif
     absorb(buf, sigma, delta);
+#ifdef FPFP_OC_PROF
+    pc_abs += clock64() - b1_;
+#endif
     ++sweeps;
     if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;
   }
+#ifdef FPFP_OC_PROF
+  if ((b == 0 || b == nb - 1) && threadIdx.x == 0)
+    printf("oc-prof block %d: %d sweeps, clk/sweep: element loop %lld, partials %lld, barrier %lld, absorb %lld\n",
+           b, sweeps, pc_rows / sweeps, pc_cols / sweeps, pc_bar / sweeps, pc_abs / sweeps);
+#endif
 
   // write the tile back in fp32 (slack persists across outer iterations, reading A3)
   for (int i = warp; i < nr; i += kWarps)
