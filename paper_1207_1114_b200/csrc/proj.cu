@@ -85,8 +85,13 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // One tile pass over rows [rb*TR, ...) x cols [cb*512, ...) of Y.
-//   kSweep = false: sums only (Z = Y).   kSweep = true: Z = max(Y + t_i - u_j, 0), written back.
-template <bool kSweep>
+//   kSweep = false: sums only (Z = Y), accumulated in fp64 (the fresh GEMM output cancels in the
+//   first correction, reading A2 / DESIGN.md §6).
+//   kSweep = true: Z = max(Y + t_i - u_j, 0) written back; the sums of Z for the next sweep are
+//   accumulated in fp32 per lane (16 values of a row, <= 64 rows of a column) and in fp64 beyond:
+//   their rounding (<= 2^-18 relative) is far below that of the fp32 storage of Y at the same sweep.
+//   kFull: every column of the tile is inside m (no per-element bounds test).
+template <bool kSweep, bool kFull = false>
 __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double sigma, float& dmax,
                                           ProjSmem& sm, Ring& ring_st) {
   const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
@@ -97,16 +102,18 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   const double inv_m = 1.0 / (double)p.m;
 
   double u[kQ][4], colacc[kQ][4];
+  float colf[kQ][4];
   bool inrow[kQ];  // float4 inside the allocated row (col < ldY)
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
     const int j0 = colbase + q * 128 + lane * 4;
-    inrow[q] = j0 < p.ldY;
+    inrow[q] = kFull || j0 < p.ldY;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int j = j0 + e;
-      u[q][e] = (kSweep && j < p.m) ? __ldcg(p.c + j) * inv_m : 0.0;
+      u[q][e] = (kSweep && (kFull || j < p.m)) ? __ldcg(p.c + j) * inv_m : 0.0;
       colacc[q][e] = 0.0;
+      colf[q][e] = 0.0f;
     }
   }
   const double tconst = (1.0 + sigma * inv_m) * inv_m;  // (1/n + 1^T Y 1 / n^2)
@@ -192,33 +199,33 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
         ti = tconst - (t < 32 ? rlo : rhi) * inv_m;
       }
       double racc = 0.0;
+      float racc_f = 0.0f;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         float* ve = reinterpret_cast<float*>(&cur[q]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int j = colbase + q * 128 + lane * 4 + e;
-          const bool valid = j < p.m;
+          const bool valid = kFull || j < p.m;
           const float y = ve[e];
-          double zz;
           if (kSweep) {
             const double zd = ((double)y + ti) - u[q][e];          // P1, fp64
-#ifdef FPFP_PROJ_SUM_STORED
-            const float z = valid ? (float)fmax(zd, 0.0) : 0.0f;    // P2, one rounding to fp32
-            zz = (double)z;
-#else
-            zz = valid ? fmax(zd, 0.0) : 0.0;                       // P2 in fp64: the sums use it
-            const float z = (float)zz;                              // one rounding to fp32 (stored)
-#endif
+            // P2 after the one rounding to fp32: rounding is monotonic and 0 is exact, so
+            // max(fl32(zd), 0) = fl32(max(zd, 0)); one FMNMX instead of an fp64 max + selects
+            float z = fmaxf((float)zd, 0.0f);
+            if (!valid) z = 0.0f;
             dmax = fmaxf(dmax, fabsf(z - y));                       // delta
             ve[e] = z;
+            racc_f += z;
+            colf[q][e] += z;
           } else {
-            zz = valid ? (double)y : 0.0;
+            const double zz = valid ? (double)y : 0.0;
+            racc += zz;
+            colacc[q][e] += zz;
           }
-          racc += zz;
-          colacc[q][e] += zz;
         }
       }
+      if (kSweep) racc = (double)racc_f;
       if (kSweep) {
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
@@ -255,7 +262,8 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
 #pragma unroll
   for (int q = 0; q < kQ; ++q)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) sm.col[warp][q * 128 + lane * 4 + e] = colacc[q][e];
+    for (int e = 0; e < 4; ++e)
+      sm.col[warp][q * 128 + lane * 4 + e] = kSweep ? (double)colf[q][e] : colacc[q][e];
   __syncthreads();
   for (int jj = threadIdx.x; jj < kProjTC; jj += kProjThreads) {
     const int j = colbase + jj;
@@ -267,6 +275,14 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
     }
   }
   __syncthreads();
+}
+
+// one sweep over a tile: the bounds-free variant when all 512 columns are inside m
+__device__ __forceinline__ void sweep_tile(const ProjArgs& p, int t, double sigma, float& dmax,
+                                           ProjSmem& sm, Ring& ring) {
+  const int cb = t - (t / p.CB) * p.CB;
+  if ((cb + 1) * kProjTC <= p.m) tile_pass<true, true>(p, t, sigma, dmax, sm, ring);
+  else tile_pass<true, false>(p, t, sigma, dmax, sm, ring);
 }
 
 // r_i = sum_cb rowpart[cb][i], c_j = sum_rb colpart[rb][j]; one warp per index: lane l sums the
@@ -473,7 +489,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   if (p.mode == kProjOneSweep) {        // one P1+P2 sweep with the global c, sigma = c[m]
     const double sigma = p.c[p.m];
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm, ring);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
@@ -526,7 +542,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   float delta = 0.0f;
   for (;;) {
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<true>(p, t, sigma, dmax, sm, ring);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
