@@ -34,6 +34,7 @@ struct __align__(1024) SmemTC {
   int8_t Wd[3][kPlane];       // X digits (GEMM1 N side), then U digits (GEMM2 N side)
   float G[kS][kLdG];          // GEMM2 output staging (row = TMEM lane)
   float colp[2][8][kS];       // per-warp column partial sums (double buffered)
+  float csum[kS];             // combined column sums of the current sweep
   float dl[2][8];
   float red[8];
   int eP[kS], eA[kS], eW[kS]; // row exponents
@@ -428,13 +429,16 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       int s = 0;
       float delta = 0.f;
       for (;;) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        // the 8 warp partials of column t combined once (threads 0..127), then read by every warp
+        if (threadIdx.x < kS) {
           float c = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) c += sm.colp[buf][w][lane + 32 * e];
-          cs[e] = c;
+          for (int w = 0; w < 8; ++w) c += sm.colp[buf][w][threadIdx.x];
+          sm.csum[threadIdx.x] = c;
         }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cs[e] = sm.csum[lane + 32 * e];
         const float sigma = warp_sum((cs[0] + cs[1]) + (cs[2] + cs[3]));
         const float tconst = (1.0f + sigma * inv_m) * inv_m;
         float cu[4];
