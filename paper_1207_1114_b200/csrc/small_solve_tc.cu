@@ -103,7 +103,8 @@ __device__ __forceinline__ void split_rows_smem(const float* src, int rows, int 
 }
 
 // The digit planes of the new X straight from the Y-tile register layout of the blend (warp w owns
-// rows 16w .. 16w + 15, lane l columns l, l + 32, l + 64, l + 96): no reload from global memory.
+// rows 16w .. 16w + 15, lane l columns 4l .. 4l + 3): no reload from global memory; the 4 digits of
+// a lane's consecutive columns go to shared memory as one packed word per plane.
 __device__ __forceinline__ void split_tile_smem(const float (&x)[16][4], int8_t (*d)[kPlane], int* ex) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -113,14 +114,12 @@ __device__ __forceinline__ void split_tile_smem(const float (&x)[16][4], int8_t 
     mx = warp_max(mx);
     const int e = frexp_exp(mx);
     if (lane == 0) ex[row] = e;
-    const float inv = exp2i(-e);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int a, b, c;
-      digits3(x[r][q], inv, a, b, c);
-      const int o = swz(row, lane + 32 * q);
-      d[0][o] = (int8_t)a; d[1][o] = (int8_t)b; d[2][o] = (int8_t)c;
-    }
+    int w1, w2, w3;
+    digits4(x[r], exp2i(-e), w1, w2, w3);
+    const int o = swz(row, 4 * lane);
+    *reinterpret_cast<int*>(&d[0][o]) = w1;
+    *reinterpret_cast<int*>(&d[1][o]) = w2;
+    *reinterpret_cast<int*>(&d[2][o]) = w3;
   }
 }
 
@@ -310,13 +309,13 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     // digit planes of the constant graphs (A' is GEMM1's M side, A is GEMM2's)
     split_rows_smem(Ap, np, np, sm.Pd, sm.eP);
     split_rows_smem(A, n, n, sm.Ad, sm.eA);
-    // Y register tile: rows 16w+r, cols l+32e
+    // Y register tile: rows 16w+r, cols 4l+e
     float y[16][4];
 #pragma unroll
     for (int r = 0; r < 16; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = lane + 32 * e;
+        const int i = warp * 16 + r, j = 4 * lane + e;
         y[r][e] = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
       }
 
@@ -327,7 +326,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     for (int r = 0; r < 16; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = lane + 32 * e;
+        const int i = warp * 16 + r, j = 4 * lane + e;
         xr[r][e] = (i < n && j < np) ? X[(int64_t)i * np + j] : 0.f;
       }
     split_tile_smem(xr, sm.Wd, sm.eW);
@@ -403,7 +402,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         const int i = warp * 16 + r;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (i < n && lane + 32 * e < np) y[r][e] = sm.G[i][lane + 32 * e];
+          if (i < n && 4 * lane + e < np) y[r][e] = sm.G[i][4 * lane + e];
       }
 
       SSP(3);
@@ -419,7 +418,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           float s = 0.f;
 #pragma unroll
           for (int r = 0; r < 16; ++r) s += yy[r][e];
-          sm.colp[buf][warp][lane + 32 * e] = s;
+          sm.colp[buf][warp][4 * lane + e] = s;
         }
       };
       sums(y);
@@ -438,7 +437,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         }
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 4; ++e) cs[e] = sm.csum[lane + 32 * e];
+        for (int e = 0; e < 4; ++e) cs[e] = sm.csum[4 * lane + e];
         const float sigma = warp_sum((cs[0] + cs[1]) + (cs[2] + cs[3]));
         const float tconst = (1.0f + sigma * inv_m) * inv_m;
         float cu[4];
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           const float ti = tconst - rs[r] * inv_m;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int j = lane + 32 * e;
+            const int j = 4 * lane + e;
             const float yo = y[r][e];
             const float z = (kFull || (i < m && j < m)) ? fmaxf((yo + ti) - cu[e], 0.f) : 0.f;  // P1, P2
             if (kDelta) dmax = fmaxf(dmax, fabsf(z - yo));
@@ -484,7 +483,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         rmx[r] = 0.f;                         // X~ >= 0: 0 is the identity of the max
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int j = lane + 32 * e;
+          const int j = 4 * lane + e;
           xt[r][e] = (1.0f - p.alpha) * xr[r][e] + p.alpha * y[r][e];
           if (i < n && j < np) rmx[r] = fmaxf(rmx[r], xt[r][e]);
         }
@@ -508,7 +507,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         const int i = warp * 16 + r;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int j = lane + 32 * e;
+          const int j = 4 * lane + e;
           if (i < n && j < np) {
             const float xn = xt[r][e] * inv_scale;
             rl = fmaxf(rl, fabsf(xn - xr[r][e]));
@@ -525,14 +524,12 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           const int row = warp * 16 + r;
           const int e = frexp_exp(rmx[r] * inv_scale);
           if (lane == 0) sm.eW[row] = e;
-          const float inv = exp2i(-e);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            int a, b, c;
-            digits3(xr[r][q], inv, a, b, c);
-            const int o = swz(row, lane + 32 * q);
-            sm.Wd[0][o] = (int8_t)a; sm.Wd[1][o] = (int8_t)b; sm.Wd[2][o] = (int8_t)c;
-          }
+          int w1, w2, w3;
+          digits4(xr[r], exp2i(-e), w1, w2, w3);   // columns 4 lane .. 4 lane + 3: packed
+          const int o = swz(row, 4 * lane);
+          *reinterpret_cast<int*>(&sm.Wd[0][o]) = w1;
+          *reinterpret_cast<int*>(&sm.Wd[1][o]) = w2;
+          *reinterpret_cast<int*>(&sm.Wd[2][o]) = w3;
         }
       }
       rl = warp_max(rl);
@@ -557,7 +554,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     for (int r = 0; r < 16; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = lane + 32 * e;
+        const int i = warp * 16 + r, j = 4 * lane + e;
         if (i < n && j < np) X[(int64_t)i * np + j] = xr[r][e];
       }
     if (p.Y) {
@@ -565,7 +562,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       for (int r = 0; r < 16; ++r)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int i = warp * 16 + r, j = lane + 32 * e;
+          const int i = warp * 16 + r, j = 4 * lane + e;
           if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = y[r][e];
         }
     }
