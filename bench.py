@@ -276,7 +276,7 @@ def run_ours(args):
     roofline = {
         "kernel": f"gemm_{precision_name(prec)}", "bound": bound, "achieved": round(achieved_tf, 2),
         "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
-        "traffic": ncu_traffic(f"gemm_{precision_name(prec)}"),
+        "traffic": ncu_traffic(f"gemm_{precision_name(prec)}") if args.workload == "c5" else None,
         "flops_per_launch": flops_launch, "ms_per_launch": round(gemm_ms, 4),
         "share_of_step": round(2 * gemm_ms / step_ms, 4), "peak_source": peak_note,
         "vs_measured_pipe": pipe,
@@ -287,14 +287,20 @@ def run_ours(args):
             "achieved": round(proj_gbs, 1), "peak": mp["hbm_gbs"], "unit": "GB/s",
             "frac": round(proj_gbs / mp["hbm_gbs"], 4), "bytes_per_launch": pbytes,
             "ms_per_launch": round(proj_ms, 4), "share_of_step": round(proj_ms / step_ms, 4),
-            "traffic": ncu_traffic("proj_kernel"), "peak_source": f"{src} hbm_gbs"},
+            "traffic": ncu_traffic("proj_kernel") if args.workload == "c5" else None,
+            "peak_source": f"{src} hbm_gbs"},
     }
 
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_desc(p, args.workload), "n": p.n, "n_prime": p.n_prime, "d": p.d,
+        "config": {"workload": (workload_desc(p, args.workload) if args.workload == "c5" else
+                                (f"c2 problem (BASELINE configs[1] recipe: n=n'={p.n}, d={p.d}, ER p=0.5, "
+                                 f"lambda={p.lam}, alpha={p.alpha}) on c5's fixed schedule: eps = 0, "
+                                 f"{inner} sweeps per outer (the converging c2 run is secondary_c2 of "
+                                 f"the default line)")),
+                   "n": p.n, "n_prime": p.n_prime, "d": p.d,
                    "inner_sweeps": inner, "gemm": precision_name(prec),
                    "parallelism": (f"rowshard{world} (NCCL all-gather of U + per-sweep all-reduce)" if sharded
                                    else ("replicas" if world > 1 else "single")),
