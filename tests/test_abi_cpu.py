@@ -46,3 +46,43 @@ def test_static_calls_without_device():
     # argument validation happens before any device call
     assert L.fastpfp_create(0, 5, 0, ctypes.byref(h)) == _native.EINVAL
     assert L.fastpfp_create(5, 5, -1, ctypes.byref(h)) == _native.EINVAL
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # the binding has no fallback: a missing libfastpfp.so is an error at first use
+    code = ("import paper_1207_1114_b200 as F\n"
+            "try:\n    F.lib()\nexcept Exception as e:\n    print('RAISED', type(e).__name__)\n"
+            "else:\n    print('LOADED')\n")
+    env = dict(os.environ, FASTPFP_LIB=str(tmp_path / "absent.so"))
+    out = subprocess.run([os.sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__)))).stdout
+    assert "RAISED" in out, out
+
+
+def test_no_device_is_an_error_not_a_cpu_fallback():
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = ctypes.c_void_p()
+    st = _native.lib().fastpfp_create(8, 8, 0, ctypes.byref(h))
+    assert st in (_native.ENODEV, _native.ECUDA), st
+
+
+def test_product_package_never_imports_the_oracle():
+    # the oracle is test infrastructure: nothing under paper_1207_1114_b200/ may import it
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1207_1114_b200")
+    offenders = []
+    for dp, _, files in os.walk(root):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dp, f)).read()
+                if "import oracle" in src or "from oracle" in src:
+                    offenders.append(os.path.join(dp, f))
+    assert not offenders, offenders
+    # and the CUDA sources share no header with it
+    csrc = os.path.join(root, "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "oracle" not in "".join(l for l in src.splitlines() if l.startswith("#include")), f
