@@ -309,7 +309,63 @@ gemm_i8_kernel(const __grid_constant__ CUtensorMap mP1, const __grid_constant__ 
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader);   // accumulators free
-      if (row < p.M) {
+      if (t + ncl >= num_tiles) {
+        // this CTA's last tile: every operand stage is idle once the accumulators are complete
+        // (no further loads are issued), so the tile is staged through shared memory and written
+        // with coalesced row stores. Matters when a CTA has few tiles (n ~ 1000: one tile each,
+        // the epilogue is the whole tail of the kernel); rows of one thread are 512 B apart.
+        if (p.epi == kEpiRowMax && row < p.M) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+        float* stile = reinterpret_cast<float*>(smem);   // [128][128] fp32, float4 c at c ^ (row & 31)
+        float* srow = stile + lrow * kTileN;
+#pragma unroll
+        for (int c4 = 0; c4 < kTileN / 4; ++c4)
+          *reinterpret_cast<float4*>(srow + ((c4 ^ (lrow & 31)) * 4)) =
+              make_float4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int col = cbase + lane * 4;    // lane l owns columns 4l .. 4l + 3 of every row
+        const bool cfull = col + 4 <= p.N;
+        const bool add_d = (p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D;
+        for (int r0 = ew; r0 < kPRows; r0 += 32) {
+          // 8 rows per batch: their lambda K (and PG X) loads are issued before any store (C may
+          // alias D as far as the compiler knows, which would serialise load / store pairs)
+          float4 dv[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int grow = rbase + r0 + 4 * u;
+            const bool ok = cfull && grow < p.M;
+            dv[u] = (add_d && ok) ? __ldg(reinterpret_cast<const float4*>(p.D + (int64_t)grow * p.ldD + col))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            xv[u] = (p.epi == kEpiPG && ok)
+                        ? __ldg(reinterpret_cast<const float4*>(p.D2 + (int64_t)grow * p.ldD2 + col))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = r0 + 4 * u;
+            const int grow = rbase + r;
+            if (grow >= p.M) break;
+            float4 v = *reinterpret_cast<const float4*>(stile + r * kTileN + ((lane ^ (r & 31)) * 4));
+            float* ve = reinterpret_cast<float*>(&v);
+            if (cfull) {
+              v.x += p.lam * dv[u].x; v.y += p.lam * dv[u].y; v.z += p.lam * dv[u].z; v.w += p.lam * dv[u].w;
+              if (p.epi == kEpiPG) {   // Projected Gradient: X + alpha (A X A' + lambda K)
+                v.x = p.scale * v.x + xv[u].x; v.y = p.scale * v.y + xv[u].y;
+                v.z = p.scale * v.z + xv[u].z; v.w = p.scale * v.w + xv[u].w;
+              }
+              *reinterpret_cast<float4*>(p.C + (int64_t)grow * p.ldC + col) = v;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                if (col + e >= p.N) break;
+                float x = ve[e];
+                if (add_d) x += p.lam * p.D[(int64_t)grow * p.ldD + col + e];
+                if (p.epi == kEpiPG) x = p.scale * x + p.D2[(int64_t)grow * p.ldD2 + col + e];
+                p.C[(int64_t)grow * p.ldC + col + e] = x;
+              }
+            }
+          }
+        }
+      } else if (row < p.M) {
         if (p.epi == kEpiRowMax) atomicMax(p.rowmax + row, __float_as_uint(rmax));
         float* crow = p.C + (int64_t)row * p.ldC + cbase;
         const bool add_d = (p.epi == kEpiAxpy || p.epi == kEpiPG) && p.D;
