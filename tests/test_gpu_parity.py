@@ -84,7 +84,7 @@ def test_gemm_nt_error_bound(prec, cg, M, N, K):
 
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (129, 257, 33), (300, 1000, 700),
                                    (1000, 1000, 1000), (256, 512, 4096), (1500, 700, 2048),
-                                   (640, 384, 16384)])
+                                   (640, 384, 16384), (2500, 2100, 96)])   # last: 170 tiles, ragged
 @pytest.mark.parametrize("signed", [False, True])
 def test_gemm_nt_int8_ozaki_error_bound(M, N, K, signed):
     # Ozaki int8 (PRECISION = 3): rows = 2^e * (3 signed 7-bit digits), digit pairs p + q <= 4
@@ -207,6 +207,18 @@ def test_config5_recipe_reduced(prec, cg):
     res = run_pair(p, prec, lockstep=6, cta_group=cg)
     assert max(res.lockstep_max) <= 1e-4 and res.final_diff <= 1e-4
     assert res.gpu_sweeps == res.oracle_sweeps == [20] * 6
+
+
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
+def test_config5_recipe_ragged_many_tiles(prec):
+    # n = 2600: 11 x 21 = 231 GEMM pair tiles (> 74 CTA pairs, so CTAs run several tiles and the
+    # int8 epilogue's register path runs as well as its staged last tile), ragged in M (40 rows) and
+    # N (40 columns), with the lambda K epilogue (d = 64); ragged projection tiles (2600 = 5 x 512 + 40)
+    p = inputs.config5(n=2600)
+    p.max_iter1 = 3
+    res = run_pair(p, prec, lockstep=3, proj_kernel=1)
+    assert max(res.lockstep_max) <= 1e-4 and res.final_diff <= 1e-4
+    assert res.gpu_sweeps == res.oracle_sweeps == [20] * 3
 
 
 # ---------------------------------------------------------------------------------------------
