@@ -69,6 +69,10 @@ struct fastpfp_handle {
   I8Buf Ai8, Api8, Xi8, Ui8, Ui8all;   // Ui8all: gathered U digit planes [world][n'][n/P] (sharded)
   unsigned* Urowmax = nullptr;
   bool i8_ready = false;
+  // Xi8 holds the digits of the current X: set by a digit split of X or by the streaming finalize
+  // that writes them (int8 path, one GPU); anything else that changes X clears it
+  bool xdig_fresh = false;
+  unsigned long long* xrowmax = nullptr;   // [n] max |X~| per row (bits), for the fused digits
   // FastGA workspace (ga.cu), allocated on first use of FASTPFP_METHOD_FASTGA
   double *ga_E = nullptr, *ga_u = nullptr, *ga_v = nullptr, *ga_dlt = nullptr, *ga_rho = nullptr;
   int64_t ga_ldE = 0;
@@ -217,6 +221,7 @@ int reset_state(fastpfp_handle* h) {
   CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
   CK(h, cudaStreamSynchronize(s));
   h->t = 0;
+  h->xdig_fresh = false;
   return FASTPFP_OK;
 }
 
@@ -254,6 +259,7 @@ int i8_prepare(fastpfp_handle* h) {
     CK(h, alloc_i8(h->Ui8, (int)h->np, (int)h->n));
     if (h->dist) CK(h, alloc_i8(h->Ui8all, (int)(h->world * h->np), (int)h->n));
     CK(h, alloc_arr(h->Urowmax, (size_t)h->np));
+    CK(h, alloc_arr(h->xrowmax, (size_t)h->n));
     h->i8_ready = true;
   }
   if (h->graphs_set) {
@@ -261,6 +267,7 @@ int i8_prepare(fastpfp_handle* h) {
     CK(h, split_i8(h->Ap, h->Api8, nullptr, nullptr, h->stream));
     CK(h, split_i8(h->X, h->Xi8, nullptr, nullptr, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
+    h->xdig_fresh = true;
   }
   return FASTPFP_OK;
 }
@@ -272,7 +279,8 @@ int run_products(fastpfp_handle* h, double lambda, float* out, int64_t ldo, int 
   cudaStream_t s = h->stream;
   const int N = (int)h->n, NP = (int)h->np;
   if (h->precision == 3) {
-    CK(h, split_i8(h->X, h->Xi8, nullptr, done, s));   // digits of the current X
+    if (!h->xdig_fresh) CK(h, split_i8(h->X, h->Xi8, nullptr, done, s));   // digits of the current X
+    h->xdig_fresh = false;   // the projection that follows changes X
     I8Gemm g1{};
     for (int k = 0; k < 3; ++k) { g1.P[k] = h->Api8.d[k]; g1.Q[k] = h->Xi8.d[k]; }
     g1.ldP = h->Api8.ld; g1.eP = h->Api8.e; g1.ldQ = h->Xi8.ld; g1.eQ = h->Xi8.e;
@@ -912,9 +920,16 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       pa.rowpart = h->rowpart; pa.colpart = h->colpart; pa.r = h->r; pa.c = h->c;
       pa.sig_part = h->sig_part; pa.dlt_part = h->dlt_part; pa.mu_part = h->mu_part;
       pa.rho_part = h->rho_part; pa.iter_out = h->iters + k; pa.done = h->done;
+      const bool fuse_digits = h->precision == 3 && h->i8_ready;
+      if (fuse_digits) {   // the finalize writes the new X's digit planes (no split_i8 of X next)
+        for (int q = 0; q < 3; ++q) pa.xd[q] = h->Xi8.d[q];
+        pa.ldxd = h->Xi8.ld; pa.xe = h->Xi8.e; pa.xrowmax = h->xrowmax;
+        CK(h, cudaMemsetAsync(h->xrowmax, 0, (size_t)N * sizeof(unsigned long long), s));
+      }
       CK(h, launch_proj(pa, h->grid, s));
       h->stats.launches += 1;
       h->stats.proj_launches += 1;
+      if (fuse_digits) h->xdig_fresh = true;
       if (h->profile) CK(h, cudaEventRecord(h->ev[3 * k + 2], s));
     }
     CK(h, cudaMemcpyAsync(h->h_iters, h->iters, chunk * sizeof(DevIter), cudaMemcpyDeviceToHost, s));

@@ -105,6 +105,9 @@ struct ProjArgs {
   double alpha, eps1, eps2;
   int max_iter2;
   int rescale, split, do_finalize, do_sums;
+  // optional (int8 path): the finalize also writes the new X's Ozaki digit planes and row exponents
+  // (what split_i8_kernel would compute from it), using per-row max |X~| gathered in the mu pass
+  int8_t* xd[3]; int64_t ldxd; int* xe; unsigned long long* xrowmax;
   int TR, RB, CB;        // sweep tiles: TR rows x 512 cols over m x m
   int RBx, CBx;          // finalize tiles over n x n'
   double* rowpart;       // [CB][rows]

@@ -394,6 +394,7 @@ __device__ __forceinline__ double finalize_mu(const ProjArgs& p) {
     const int rb = t / p.CBx, cb = t - (t / p.CBx) * p.CBx;
     const int row1 = min(p.n, (rb + 1) * p.TR);
     for (int i = rb * p.TR + warp; i < row1; i += kWarps) {
+      double rmx = 0.0;   // max |X~| of this row segment (for the fused digit planes)
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         const int j0 = cb * kProjTC + q * 128 + lane * 4;
@@ -404,7 +405,16 @@ __device__ __forceinline__ double finalize_mu(const ProjArgs& p) {
         const float* ye = reinterpret_cast<const float*>(&yv);
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (j0 + e < p.np) mu_loc = fmax(mu_loc, b * (double)xe[e] + a * (double)ye[e]);
+          if (j0 + e < p.np) {
+            const double xt = b * (double)xe[e] + a * (double)ye[e];
+            mu_loc = fmax(mu_loc, xt);
+            rmx = fmax(rmx, fabs(xt));
+          }
+      }
+      if (p.xrowmax) {
+        rmx = warp_max(rmx);
+        // nonnegative doubles order as their bit patterns
+        if (lane == 0) atomicMax(p.xrowmax + i, (unsigned long long)__double_as_longlong(rmx));
       }
     }
   }
@@ -424,6 +434,16 @@ __device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
     const int rb = t / p.CBx, cb = t - (t / p.CBx) * p.CBx;
     const int row1 = min(p.n, (rb + 1) * p.TR);
     for (int i = rb * p.TR + warp; i < row1; i += kWarps) {
+      // fused digits of the new X (int8 path): the row's scale is the exponent of
+      // max_j |fl32(X~_ij / mu)| = fl32(max_j |X~_ij| / mu) (rounding is monotonic), i.e. exactly
+      // what split_i8_kernel would derive from the stored row
+      float dinv = 0.0f;
+      if (p.xd[0]) {
+        const float rmax = (float)(__longlong_as_double((long long)p.xrowmax[i]) * rcp);
+        const int ex = frexp_exp(rmax);
+        dinv = exp2i(-ex);
+        if (cb == 0 && lane == 0) p.xe[i] = ex;
+      }
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         const int j0 = cb * kProjTC + q * 128 + lane * 4;
@@ -449,6 +469,18 @@ __device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
           se[e] = tf32_rna(xn - be[e]);
         }
         *reinterpret_cast<float4*>(xp) = xv;
+        if (p.xd[0]) {   // 4 consecutive columns -> one packed word per digit plane
+          int a4[4], b4[4], c4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ozaki_digits3(xe[e], dinv, a4[e], b4[e], c4[e]);
+          const int64_t o = (int64_t)i * p.ldxd + j0;
+          auto pk = [](const int (&d)[4]) {
+            return (d[0] & 0xFF) | ((d[1] & 0xFF) << 8) | ((d[2] & 0xFF) << 16) | ((d[3] & 0xFF) << 24);
+          };
+          *reinterpret_cast<int*>(p.xd[0] + o) = pk(a4);
+          *reinterpret_cast<int*>(p.xd[1] + o) = pk(b4);
+          *reinterpret_cast<int*>(p.xd[2] + o) = pk(c4);
+        }
         if (p.split) {
           *reinterpret_cast<float4*>(p.Xb + (int64_t)i * p.ldX + j0) = bv;
           *reinterpret_cast<float4*>(p.Xs + (int64_t)i * p.ldX + j0) = sv;
