@@ -279,7 +279,8 @@ int run_products(fastpfp_handle* h, double lambda, float* out, int64_t ldo, int 
   cudaStream_t s = h->stream;
   const int N = (int)h->n, NP = (int)h->np;
   if (h->precision == 3) {
-    if (!h->xdig_fresh) CK(h, split_i8(h->X, h->Xi8, nullptr, done, s));   // digits of the current X
+    const bool split_x = !h->xdig_fresh;
+    if (split_x) CK(h, split_i8(h->X, h->Xi8, nullptr, done, s));   // digits of the current X
     h->xdig_fresh = false;   // the projection that follows changes X
     I8Gemm g1{};
     for (int k = 0; k < 3; ++k) { g1.P[k] = h->Api8.d[k]; g1.Q[k] = h->Xi8.d[k]; }
@@ -300,7 +301,7 @@ int run_products(fastpfp_handle* h, double lambda, float* out, int64_t ldo, int 
     g2.D2 = h->X.p; g2.ldD2 = h->X.ld; g2.scale = (float)alpha;
     g2.done = done;
     CK(h, launch_gemm_i8(g2, s, h->device));
-    h->stats.launches += 4;
+    h->stats.launches += split_x ? 4 : 3;
     h->stats.gemm_launches += 2;
     return FASTPFP_OK;
   }
