@@ -149,12 +149,14 @@ def workload_desc(p, workload):
             f"eps1=eps2={p.eps1}, I0=I1={p.max_iter1}")
 
 
-def proj_bytes_per_outer(n, npr, sweeps, prec=0):
+def proj_bytes_per_outer(n, npr, sweeps, prec=0, fused_digits=False):
     """Algorithmic HBM bytes of one projection launch: the sums pass reads Y
     (4 m^2), each sweep reads + writes Y (8 m^2), the finalize reads X and Y[0:n,0:n'] twice and
-    writes X (4 * 5 n n') plus, for the TF32 GEMMs, X's TF32 split (another 4 * 2 n n')."""
+    writes X (4 * 5 n n') plus, for the TF32 GEMMs, X's TF32 split (another 4 * 2 n n'), or on the
+    single-GPU int8 path X's three digit planes (3 n n')."""
     m = max(n, npr)
-    return 4 * m * m + 8 * m * m * sweeps + (20 if prec == 3 else 28) * n * npr
+    fin = 28 if prec != 3 else (23 if fused_digits else 20)
+    return 4 * m * m + 8 * m * m * sweeps + fin * n * npr
 
 
 def precision_name(prec):
@@ -262,7 +264,8 @@ def run_ours(args):
     peak, bound, peak_note = gemm_peak(mp, src, prec)
     proj_ms = st["proj_ms"] / max(st["proj_launches"], 1)
     rows_local = shard.rows if sharded else p.n
-    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner, prec) * rows_local // p.n
+    fused = prec == 3 and not sharded and not st.get("onchip_launches", 0)   # streaming finalize writes X digits
+    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner, prec, fused_digits=fused) * rows_local // p.n
     proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
     step_ms = ms / args.steps
     # the same kernel against the tcgen05 issue rate measured on this part (8192 int8 / 2048 TF32
