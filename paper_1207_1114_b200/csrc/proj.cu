@@ -462,7 +462,9 @@ __device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
           if (j0 + e < p.np) {
             const double xt = b * (double)xe[e] + a * (double)ye[e];
             xn = (float)(xt * rcp);
-            rho_loc = fmaxf(rho_loc, (float)fabs((double)xn - (double)xe[e]));
+            // fl32(|xn - xo|) directly in fp32: IEEE subtraction rounds the exact difference, the
+            // same value the former fp64 difference rounded to fp32 gave (2 conversions fewer)
+            rho_loc = fmaxf(rho_loc, fabsf(xn - xe[e]));
           }
           xe[e] = xn;
           be[e] = tf32_rna(xn);

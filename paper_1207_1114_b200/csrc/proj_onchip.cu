@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       const float xo = p.X[o];
       const double xt = bb * (double)xo + a * tile[i * kLdt + j];
       const float xn = (float)(xt * rcp);
-      rho_loc = fmaxf(rho_loc, (float)fabs((double)xn - (double)xo));
+      rho_loc = fmaxf(rho_loc, fabsf(xn - xo));   // = fl32(|xn - xo|), as the fp64 difference rounded
       p.X[o] = xn;
       const float hb = tf32_rna(xn);
       p.Xb[o] = hb;
