@@ -611,6 +611,26 @@ def run_c4(args):
         dist.destroy_process_group()
 
 
+def reference_config(workload):
+    """The workload description our arm prints in its config, plus what ran."""
+    from paper_1207_1114_b200 import inputs
+    if workload == "c4":
+        cfg = {"workload": ("c4 (BASELINE configs[3]): 8192 pairs n=n'=128, ER p=0.3, noise N(0,0.02^2), "
+                            "lambda=0, 20 sweeps per outer, one pair per CTA, pairs split evenly over ranks")}
+    elif workload == "c5":
+        p = inputs.config5(n=64)   # the recipe's scalars (lambda, alpha, sweeps); sizes are c5's
+        cfg = {"workload": workload_desc(p, "c5").replace("n=n'=64", "n=n'=16384"),
+               "n": 16384, "n_prime": 16384, "d": p.d, "inner_sweeps": p.max_iter2}
+    else:
+        p = inputs.config2()
+        cfg = {"workload": (f"c2 problem (BASELINE configs[1] recipe: n=n'={p.n}, d={p.d}, ER p=0.5, "
+                            f"lambda={p.lam}, alpha={p.alpha}) on c5's fixed schedule: eps = 0, 20 sweeps per "
+                            f"outer"),
+               "n": p.n, "n_prime": p.n_prime, "d": p.d, "inner_sweeps": 20}
+    cfg["reference"] = "fp64 numpy oracle (oracle/) on host cores, bounded sample scaled to the workload"
+    return cfg
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -624,7 +644,7 @@ def run_reference(args):
     out = {"metric": METRIC, "value": round(value, 6), "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": args.workload, "reference": "fp64 numpy oracle (oracle/fastpfp.py) on host cores"},
+           "config": reference_config(args.workload),
            "cpu_baseline": {"value": round(value, 6), "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": round(value, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
