@@ -55,6 +55,19 @@ def test_pg_lockstep_vs_oracle(prec, pk, shape):
     assert res.final_diff <= 1e-4
 
 
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
+def test_pg_many_ragged_tiles(prec):
+    # n = 2600 (231 ragged GEMM pair tiles): the PG epilogue (X + alpha (A X A' + lambda K)) on the
+    # int8 kernel's register path as well as its staged last tile; streaming projection
+    p = inputs.config5(n=2600)
+    p.alpha = 0.01
+    p.max_iter1 = 2
+    p.max_iter2 = 10
+    res = run_pair(p, prec, lockstep=2, proj_kernel=1, method=1)
+    assert max(res.lockstep_max) <= 1e-4, res.lockstep_max
+    assert res.final_diff <= 1e-4
+
+
 def test_pg_dist_world1():
     import paper_1207_1114_b200 as F
     p = inputs.config5(n=1024, d=8)
