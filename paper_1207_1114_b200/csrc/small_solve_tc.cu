@@ -23,26 +23,38 @@ namespace {
 
 using namespace tc;
 
-constexpr int kT = 256;       // threads
+#ifndef FPFP_SS_THREADS
+#define FPFP_SS_THREADS 512
+#endif
+constexpr int kT = FPFP_SS_THREADS;   // threads (256 or 512)
 constexpr int kS = 128;       // max n, n', m
+constexpr int kW = kT / 32;   // warps
+constexpr int kRW = kS / kW;  // rows of the Y / X register tiles per warp (8 at 512 threads)
+constexpr int kEC = kS / (kW / 4);    // epilogue columns per warp (TMEM lane quarter = warp & 3)
 constexpr int kLdG = kS + 4;  // fp32 staging row stride
 constexpr int kPlane = kS * kS;   // one digit plane: 128 rows x 128 bytes
+static_assert(kT == 256 || kT == 512, "256 or 512 threads");
 
 struct __align__(1024) SmemTC {
   int8_t Pd[3][kPlane];       // A' digit planes (GEMM1 M side)
   int8_t Ad[3][kPlane];       // A digit planes (GEMM2 M side)
   int8_t Wd[3][kPlane];       // X digits (GEMM1 N side), then U digits (GEMM2 N side)
-  float G[kS][kLdG];          // GEMM2 output staging (row = TMEM lane)
-  float colp[2][8][kS];       // per-warp column partial sums (double buffered)
+  float G[kS][kLdG];          // product staging (row = TMEM lane); during the sweeps it holds
+                              // the per-warp column partial sums colp[2][kW][kS] (double buffered)
   float csum[kS];             // combined column sums of the current sweep
-  float dl[2][8];
-  float red[8];
+  float dl[2][kW];
+  float red[kW];
   int eP[kS], eA[kS], eW[kS]; // row exponents
-  float wmax[2][kS];          // row |max| of U per column half
+  float wmax[kW / 4][kS];     // row |max| of U per epilogue column group
   float cscale[kS];           // 2^(e_col - 14) of the N side of the current product
   uint64_t bar;               // MMA completion
   uint32_t tmem_base;
 };
+
+static_assert(sizeof(float) * 2 * kW * kS <= sizeof(float) * kS * kLdG, "colp fits in G");
+__device__ __forceinline__ float (*colp_of(SmemTC& sm))[kW][kS] {
+  return reinterpret_cast<float (*)[kW][kS]>(&sm.G[0][0]);
+}
 
 __device__ __forceinline__ float pow2(int e) {
   return (e > -127 && e < 128) ? __int_as_float((e + 127) << 23) : ldexpf(1.0f, e);
@@ -105,11 +117,11 @@ __device__ __forceinline__ void split_rows_smem(const float* src, int rows, int 
 // The digit planes of the new X straight from the Y-tile register layout of the blend (warp w owns
 // rows 16w .. 16w + 15, lane l columns 4l .. 4l + 3): no reload from global memory; the 4 digits of
 // a lane's consecutive columns go to shared memory as one packed word per plane.
-__device__ __forceinline__ void split_tile_smem(const float (&x)[16][4], int8_t (*d)[kPlane], int* ex) {
+__device__ __forceinline__ void split_tile_smem(const float (&x)[kRW][4], int8_t (*d)[kPlane], int* ex) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int row = warp * 16 + r;
+  for (int r = 0; r < kRW; ++r) {
+    const int row = warp * kRW + r;
     float mx = fmaxf(fmaxf(fabsf(x[r][0]), fabsf(x[r][1])), fmaxf(fabsf(x[r][2]), fabsf(x[r][3])));
     mx = warp_max(mx);
     const int e = frexp_exp(mx);
@@ -162,27 +174,27 @@ __device__ __forceinline__ void issue_product(const int8_t (*P)[kPlane], const i
 __device__ __forceinline__ float product_to_smem(uint32_t tmem, float rscale, const float* cscale,
                                                  float* dst) {
   const int warp = threadIdx.x >> 5;
-  const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
+  const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kEC);
   float mx = 0.0f;
 #pragma unroll 1
-  for (int h = 0; h < 2; ++h) {
-    uint32_t a2[32], a3[32], a4[32];
-    tmem_ld32_nowait(tb + (uint32_t)(h * 32), a2);
-    tmem_ld32_nowait(tb + 128u + (uint32_t)(h * 32), a3);
-    tmem_ld32_nowait(tb + 256u + (uint32_t)(h * 32), a4);
+  for (int h = 0; h < kEC / 16; ++h) {   // 16 columns at a time (48 registers of accumulators)
+    uint32_t a2[16], a3[16], a4[16];
+    tmem_ld16_nowait(tb + (uint32_t)(h * 16), a2);
+    tmem_ld16_nowait(tb + 128u + (uint32_t)(h * 16), a3);
+    tmem_ld16_nowait(tb + 256u + (uint32_t)(h * 16), a4);
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
+    for (int j = 0; j < 16; j += 4) {
       float o[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const int col = (warp >> 2) * 64 + h * 32 + j + t;
+        const int col = (warp >> 2) * kEC + h * 16 + j + t;
         float v = fmaf((float)(int)a4[j + t], 0.0078125f, (float)(int)a3[j + t]);
         v = fmaf(v, 0.0078125f, (float)(int)a2[j + t]);
         o[t] = (v * rscale) * cscale[col];
         mx = fmaxf(mx, fabsf(o[t]));
       }
-      *reinterpret_cast<float4*>(dst + h * 32 + j) = make_float4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<float4*>(dst + h * 16 + j) = make_float4(o[0], o[1], o[2], o[3]);
     }
   }
   return mx;
@@ -274,6 +286,48 @@ __device__ __forceinline__ void rows_allreduce16(float (&v)[16]) {
   }
 }
 
+// 8-row versions (16 warps x 8 rows): three halving exchanges leave the lanes whose bits 4..2
+// equal a row's index with partials of that row; xor 2 and 1 finish them, then a broadcast
+template <bool kMax>
+__device__ __forceinline__ void rows_all8(float (&v)[8]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
+  float a[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? v[k] : v[4 + k], keep = hi ? v[4 + k] : v[k];
+      a[k] = op(keep, __shfl_xor_sync(F, send, 16));
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? a[k] : a[2 + k], keep = hi ? a[2 + k] : a[k];
+      b2[k] = op(keep, __shfl_xor_sync(F, send, 8));
+    }
+  }
+  {
+    const bool hi = lane & 4;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = op(keep, __shfl_xor_sync(F, send, 4));
+  }
+  b1 = op(b1, __shfl_xor_sync(F, b1, 2));
+  b1 = op(b1, __shfl_xor_sync(F, b1, 1));
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int src = (((r >> 2) & 1) << 4) | (((r >> 1) & 1) << 3) | ((r & 1) << 2);
+    v[r] = __shfl_sync(F, b1, src);
+  }
+}
+__device__ __forceinline__ void rows_allreduce(float (&v)[16]) { rows_allreduce16(v); }
+__device__ __forceinline__ void rows_allreduce(float (&v)[8]) { rows_all8<false>(v); }
+__device__ __forceinline__ void rows_allmax(float (&v)[16]) { rows_allmax16(v); }
+__device__ __forceinline__ void rows_allmax(float (&v)[8]) { rows_all8<true>(v); }
+
 }  // namespace
 
 template <bool kFull, bool kDelta>
@@ -283,8 +337,9 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = p.n, np = p.np, m = p.m;
   const float inv_m = 1.0f / (float)m;
-  // epilogue geometry: row = TMEM lane 32 (warp & 3) + lane, columns 64 (warp >> 2) ..
-  const int erow = (warp & 3) * 32 + lane, ecol0 = (warp >> 2) * 64;
+  // epilogue geometry: row = TMEM lane 32 (warp & 3) + lane, columns kEC (warp >> 2) ..
+  const int erow = (warp & 3) * 32 + lane, ecol0 = (warp >> 2) * kEC;
+  float (*colp)[kW][kS] = colp_of(sm);
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.bar, 1);
@@ -309,24 +364,24 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     // digit planes of the constant graphs (A' is GEMM1's M side, A is GEMM2's)
     split_rows_smem(Ap, np, np, sm.Pd, sm.eP);
     split_rows_smem(A, n, n, sm.Ad, sm.eA);
-    // Y register tile: rows 16w+r, cols 4l+e
-    float y[16][4];
+    // Y register tile: rows kRW w + r, cols 4l + e
+    float y[kRW][4];
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < kRW; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = 4 * lane + e;
+        const int i = warp * kRW + r, j = 4 * lane + e;
         y[r][e] = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
       }
 
     int it = 0, conv = 0, total_sweeps = 0, degen = 0;
     float rho = 0.f;
-    float xr[16][4];            // X in the Y-tile layout (kept for the blend and the next digits)
+    float xr[kRW][4];           // X in the Y-tile layout (kept for the blend and the next digits)
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < kRW; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = 4 * lane + e;
+        const int i = warp * kRW + r, j = 4 * lane + e;
         xr[r][e] = (i < n && j < np) ? X[(int64_t)i * np + j] : 0.f;
       }
     split_tile_smem(xr, sm.Wd, sm.eW);
@@ -358,12 +413,14 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       tc_fence_before();
       __syncthreads();                                     // U staged; X digits / exps consumed
       {
-        const float rmx = fmaxf(sm.wmax[0][erow], sm.wmax[1][erow]);
+        float rmx = sm.wmax[0][erow];
+#pragma unroll
+        for (int g = 1; g < kW / 4; ++g) rmx = fmaxf(rmx, sm.wmax[g][erow]);
         const int e = frexp_exp(rmx);
         if (warp < 4) sm.eW[erow] = e;
         const float inv = exp2i(-e);
 #pragma unroll 4
-        for (int j = 0; j < 64; j += 4) {
+        for (int j = 0; j < kEC; j += 4) {
           const float4 g = *reinterpret_cast<const float4*>(&sm.G[erow][ecol0 + j]);
           const float q[4] = {g.x, g.y, g.z, g.w};
           int w1, w2, w3;
@@ -391,35 +448,39 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       __syncthreads();
       product_to_smem(tmem, pow2(sm.eA[erow]), sm.cscale, &sm.G[erow][ecol0]);   // G staged
       if (Kp && erow < n) {                               // + lambda K (line 3)
-        for (int j = 0; j < 64 && ecol0 + j < np; ++j)
+        for (int j = 0; j < kEC && ecol0 + j < np; ++j)
           sm.G[erow][ecol0 + j] += p.lam * Kp[(int64_t)erow * np + ecol0 + j];
       }
       tc_fence_before();
       __syncthreads();
       // Y[0:n, 0:n'] = G ; slack entries keep their values (reading A3)
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int i = warp * 16 + r;
+      for (int r = 0; r < kRW; ++r) {
+        const int i = warp * kRW + r;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           if (i < n && 4 * lane + e < np) y[r][e] = sm.G[i][4 * lane + e];
       }
+      __syncthreads();   // G is read; the column partials of the sweeps reuse its space
 
       SSP(3);
       // ---- projection loop (P1 + P2 per sweep), sums of the current Y first (as small_solve.cu)
       int buf = 0;
-      float rs[16], cs[4];
-      auto sums = [&](float (&yy)[16][4]) {
+      float rs[kRW], cs[4];
+      auto sums = [&](float (&yy)[kRW][4]) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) rs[r] = (yy[r][0] + yy[r][1]) + (yy[r][2] + yy[r][3]);
-        rows_allreduce16(rs);
+        for (int r = 0; r < kRW; ++r) rs[r] = (yy[r][0] + yy[r][1]) + (yy[r][2] + yy[r][3]);
+        rows_allreduce(rs);
+        float4 cv;
+        float* ce = reinterpret_cast<float*>(&cv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float s = 0.f;
 #pragma unroll
-          for (int r = 0; r < 16; ++r) s += yy[r][e];
-          sm.colp[buf][warp][4 * lane + e] = s;
+          for (int r = 0; r < kRW; ++r) s += yy[r][e];
+          ce[e] = s;
         }
+        *reinterpret_cast<float4*>(&colp[buf][warp][4 * lane]) = cv;
       };
       sums(y);
       float dmax = 0.f;
@@ -428,11 +489,11 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       int s = 0;
       float delta = 0.f;
       for (;;) {
-        // the 8 warp partials of column t combined once (threads 0..127), then read by every warp
+        // the kW warp partials of column t combined once (threads 0..127), then read by every warp
         if (threadIdx.x < kS) {
           float c = 0.f;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) c += sm.colp[buf][w][threadIdx.x];
+          for (int w = 0; w < kW; ++w) c += colp[buf][w][threadIdx.x];
           sm.csum[threadIdx.x] = c;
         }
         __syncthreads();
@@ -446,8 +507,8 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         buf ^= 1;
         dmax = 0.f;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const int i = warp * 16 + r;
+        for (int r = 0; r < kRW; ++r) {
+          const int i = warp * kRW + r;
           const float ti = tconst - rs[r] * inv_m;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -467,7 +528,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         delta = 0.f;
         if (kDelta) {
 #pragma unroll
-          for (int w = 0; w < 8; ++w) delta = fmaxf(delta, sm.dl[buf][w]);
+          for (int w = 0; w < kW; ++w) delta = fmaxf(delta, sm.dl[buf][w]);
         }
         ++s;
         if (delta < p.eps2 || s >= p.max_iter2) break;
@@ -476,10 +537,10 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       SSP(4);
 
       // ---- blend + rescale (lines 8-9) on X (registers), row maxima for the next X digits
-      float xt[16][4], rmx[16];
+      float xt[kRW][4], rmx[kRW];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int i = warp * 16 + r;
+      for (int r = 0; r < kRW; ++r) {
+        const int i = warp * kRW + r;
         rmx[r] = 0.f;                         // X~ >= 0: 0 is the identity of the max
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -488,23 +549,23 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           if (i < n && j < np) rmx[r] = fmaxf(rmx[r], xt[r][e]);
         }
       }
-      rows_allmax16(rmx);
+      rows_allmax(rmx);
       float mu = rmx[0];
 #pragma unroll
-      for (int r = 1; r < 16; ++r) mu = fmaxf(mu, rmx[r]);
+      for (int r = 1; r < kRW; ++r) mu = fmaxf(mu, rmx[r]);
       if (lane == 0) sm.red[warp] = mu;
       __syncthreads();
       mu = 0.f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) mu = fmaxf(mu, sm.red[w]);
+      for (int w = 0; w < kW; ++w) mu = fmaxf(mu, sm.red[w]);
       __syncthreads();
       if (!(mu > 1e-30f)) { degen = 1; break; }   // degenerate guard (reading A7), X unchanged
       // X / max X as a product with the reciprocal (<= 1 ulp from the quotient)
       const float inv_scale = p.rescale ? 1.0f / mu : 1.0f;
       float rl = 0.f;
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int i = warp * 16 + r;
+      for (int r = 0; r < kRW; ++r) {
+        const int i = warp * kRW + r;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int j = 4 * lane + e;
@@ -520,8 +581,8 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       // and the division are monotonic, so this is the max of the stored values)
       {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const int row = warp * 16 + r;
+        for (int r = 0; r < kRW; ++r) {
+          const int row = warp * kRW + r;
           const int e = frexp_exp(rmx[r] * inv_scale);
           if (lane == 0) sm.eW[row] = e;
           int w1, w2, w3;
@@ -537,7 +598,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       __syncthreads();
       rho = 0.f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) rho = fmaxf(rho, sm.red[w]);
+      for (int w = 0; w < kW; ++w) rho = fmaxf(rho, sm.red[w]);
       __syncthreads();
       ++it;
       SSP(5);
@@ -551,18 +612,18 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 
     // write back X (and Y when slack exists)
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < kRW; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int i = warp * 16 + r, j = 4 * lane + e;
+        const int i = warp * kRW + r, j = 4 * lane + e;
         if (i < n && j < np) X[(int64_t)i * np + j] = xr[r][e];
       }
     if (p.Y) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
+      for (int r = 0; r < kRW; ++r)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int i = warp * 16 + r, j = 4 * lane + e;
+          const int i = warp * kRW + r, j = 4 * lane + e;
           if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = y[r][e];
         }
     }
