@@ -82,7 +82,8 @@ typedef enum fastpfp_option {
    *     Algorithm 1 initialises Y once and only overwrites Y[0:n,0:n'], reading A3.
    * 1 = reset: slack set to 0 before every projection (SPEC's variant). */
   FASTPFP_OPT_SLACK_MODE = 1,
-  /* 0 = 3xTF32 tensor-core GEMMs (tcgen05; fp32-accurate, default)
+  /* Default: 3 where it applies (n, n' <= 32768; sharded: (n/P) % 128 == 0), else 0.
+   * 0 = 3xTF32 tensor-core GEMMs (tcgen05; fp32-accurate)
    * 1 = 1xTF32 tensor-core GEMMs (reported separately; NOT parity-accurate)
    * 2 = fp32 SIMT GEMMs (FFMA; the scaffold the tensor-core path is checked against)
    * 3 = Ozaki int8 tensor-core GEMMs (tcgen05 kind::i8; every operand row = a power-of-two scale
@@ -90,7 +91,8 @@ typedef enum fastpfp_option {
    *     classes; fp32-accurate). Needs n, n' <= 32768 (exact int32 class sums);
    *     sharded handles need (n/P) % 128 == 0 (else
    *     EUNSUPPORTED); allocates 3 bytes per element of A, A', X, U (+ U in fp32) on first
-   *     selection. Sharded: the row scales of U are all-reduced (MAX) and U's digit planes, not its
+   *     selection. Switching precision after set_graphs re-derives the operand form the new
+   *     precision reads (digit planes or TF32 parts of A, A' and the current X). Sharded: the row scales of U are all-reduced (MAX) and U's digit planes, not its
    *     TF32 parts, are all-gathered (3 instead of 8 bytes per element). */
   FASTPFP_OPT_PRECISION = 2,
   /* 1 (default) = X <- X/max(X) each iteration; 0 = off (Theorem 1 test, reading A11). */
@@ -178,8 +180,18 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
 /* Copy the current X (n x n') to dst (host if dst_is_device == 0, else device memory). */
 int fastpfp_copy_x(fastpfp_handle* h, float* dst, int dst_is_device);
 
-/* Copy the current slacked matrix Y (m x m, m = max(n, n')) to dst (diagnostics and tests). */
+/* Copy the current slacked matrix Y to dst (diagnostics, tests, checkpoints): m x m with
+ * m = max(n, n') on a single-GPU handle; on a row-sharded handle the LOCAL rows, n/P x m. After an
+ * outer iteration Y holds the last projection output; its slack part (columns n'..m-1 when n > n',
+ * rows n..m-1 when n < n') is the state Algorithm 1 carries into the next iteration. */
 int fastpfp_copy_y(fastpfp_handle* h, float* dst, int dst_is_device);
+
+/* Checkpoint/resume of the slack: load Y (same shape as fastpfp_copy_y writes, finite,
+ * else ENONFINITE) into the handle without touching X. Algorithm 1 initialises Y once and
+ * overwrites only Y[0:n, 0:n'] each iteration, so a run resumed with
+ * fastpfp_set_x0(X_saved) followed by fastpfp_set_y(Y_saved) continues exactly as the original
+ * (set_x0 zeroes Y, so set_y must come after it). Errors: EINVAL, ESTATE (before set_graphs). */
+int fastpfp_set_y(fastpfp_handle* h, const float* Y, int is_device);
 
 /* Greedy discretization of the current X (Algorithm 1 line 11): repeatedly take the
  * largest remaining X_ij (ties: smaller i, then smaller j, reading A12) and strike row i and

@@ -99,6 +99,7 @@ def lib():
         "fastpfp_iterate": (C.c_int, [H, D, D, D, D, I32, I32, FP, C.POINTER(Report)]),
         "fastpfp_copy_x": (C.c_int, [H, FP, C.c_int]),
         "fastpfp_copy_y": (C.c_int, [H, FP, C.c_int]),
+        "fastpfp_set_y": (C.c_int, [H, FP, C.c_int]),
         "fastpfp_discretize": (C.c_int, [H, VP]),
         "fastpfp_objective": (C.c_int, [H, D, C.POINTER(D)]),
         "fastpfp_set_option": (C.c_int, [H, C.c_int, I64]),
@@ -275,11 +276,20 @@ class Solver:
         _check(lib().fastpfp_copy_x(self._h, p, dev), self._h)
         return out
 
+    def _y_shape(self):
+        m = max(self.n_glob, self.n_prime)
+        return (self.n if self.world > 1 else m, m)     # sharded: local rows x m
+
     def copy_y(self):
-        m = max(self.n, self.n_prime)
-        out = np.empty((m, m), np.float32)
+        out = np.empty(self._y_shape(), np.float32)
         _check(lib().fastpfp_copy_y(self._h, out.ctypes.data, 0), self._h)
         return out
+
+    def set_y(self, Y):
+        """Load the slacked matrix (checkpoint/resume; after set_x0, which zeroes Y)."""
+        self._check_shape(Y, self._y_shape())
+        p, dev, keep = _ptr(Y)
+        _check(lib().fastpfp_set_y(self._h, p, dev), self._h)
 
     def stats(self) -> dict:
         st = Stats()

@@ -83,6 +83,7 @@ struct fastpfp_handle {
   int* done = nullptr;            // device flag
   int* flags = nullptr;           // validation flags (device)
   double* scal = nullptr;         // device scalars (objective)
+  double* dot_part = nullptr;     // [kDotBlocks][2] objective partials (lazy)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int slack_mode = 0, precision = 0, rescale = 1, check_every = 4, cta_group = 2, method = 0;
@@ -206,6 +207,21 @@ int run_gemm(fastpfp_handle* h, GemmArgs& g) {
   return FASTPFP_OK;
 }
 
+// The TF32 GEMMs (precision 0, 1) read pre-split operands (A, A', X -> big + small parts); the
+// int8 path reads digit planes instead and the SIMT path the plain fp32 matrices.
+bool uses_tf32_split(const fastpfp_handle* h) { return h->precision == 0 || h->precision == 1; }
+
+// TF32 splits of the graphs and of the current X (set_graphs, or a switch to a TF32 precision:
+// while another precision ran, X changed without its split being refreshed)
+int tf32_prepare(fastpfp_handle* h) {
+  cudaStream_t s = h->stream;
+  CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n_glob, s));
+  CK(h, launch_split(h->Ap.p, h->Ap.ld, h->Apb.p, h->Aps.p, h->Ap.ld, (int)h->np, (int)h->np, s));
+  CK(h, launch_split(h->X.p, h->X.ld, h->Xb.p, h->Xs.p, h->X.ld, (int)h->n, (int)h->np, s));
+  CK(h, cudaStreamSynchronize(s));
+  return FASTPFP_OK;
+}
+
 // X <- X0, split, Y <- 0, t <- 0
 int reset_state(fastpfp_handle* h) {
   cudaStream_t s = h->stream;
@@ -216,7 +232,8 @@ int reset_state(fastpfp_handle* h) {
     CK(h, launch_fill(h->X.p, h->X.ld, (int)h->n, (int)h->np,
                       (float)(1.0 / ((double)h->n_glob * (double)h->np)), s));  // 11^T/(nn')
   }
-  CK(h, launch_split(h->X.p, h->X.ld, h->Xb.p, h->Xs.p, h->X.ld, (int)h->n, (int)h->np, s));
+  if (uses_tf32_split(h))
+    CK(h, launch_split(h->X.p, h->X.ld, h->Xb.p, h->Xs.p, h->X.ld, (int)h->n, (int)h->np, s));
   CK(h, cudaMemsetAsync(h->Y.p, 0, (size_t)h->yrows * h->Y.ld * sizeof(float), s));  // Y = 0
   CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), s));
   CK(h, cudaStreamSynchronize(s));
@@ -394,7 +411,7 @@ void fastpfp_destroy(fastpfp_handle* h) {
   if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
-                  (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal,
+                  (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal, (void*)h->dot_part,
                   (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
                   (void*)h->oc_bar, (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
                   (void*)h->ga_dlt, (void*)h->ga_rho})
@@ -404,6 +421,10 @@ void fastpfp_destroy(fastpfp_handle* h) {
     for (auto& e : h->ev) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
+}
+
+static bool int8_default_ok(const fastpfp_handle* h) {
+  return h->n_glob <= 32768 && h->np <= 32768 && (!h->dist || h->n % 128 == 0);
 }
 
 static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int world,
@@ -478,6 +499,12 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
       if (h->nccl->CommInitRank(&h->comm, world, id, rank) != ncclSuccess) rc = FASTPFP_ENCCL;
     }
   }
+  if (rc == FASTPFP_OK && int8_default_ok(h)) {
+    // default precision: the Ozaki int8 products (fp32-accurate) wherever they apply;
+    // 3xTF32 otherwise (n or n' > 32768, or a row shard that is not a multiple of 128 rows)
+    h->precision = 3;
+    rc = i8_prepare(h);   // allocation only: the graphs are not set yet
+  }
   if (rc != FASTPFP_OK) {
     cudaGetLastError();
     fastpfp_destroy(h);
@@ -524,7 +551,9 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
         h->precision = 3;
         return i8_prepare(h);
       }
-      h->precision = (int)value; return FASTPFP_OK;
+      h->precision = (int)value;
+      if (h->graphs_set && uses_tf32_split(h)) return tf32_prepare(h);
+      return FASTPFP_OK;
     case FASTPFP_OPT_RESCALE:
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
       h->rescale = (int)value; return FASTPFP_OK;
@@ -596,8 +625,10 @@ int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, 
   CK(h, launch_check_sym(h->Ap.p, h->Ap.ld, (int)h->np, h->flags, s));
   rc = check_flags(h, "A'");
   if (rc) return rc;
-  CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n_glob, s));
-  CK(h, launch_split(h->Ap.p, h->Ap.ld, h->Apb.p, h->Aps.p, h->Ap.ld, (int)h->np, (int)h->np, s));
+  if (uses_tf32_split(h)) {
+    CK(h, launch_split(h->A.p, h->A.ld, h->Ab.p, h->As.p, h->A.ld, (int)h->n, (int)h->n_glob, s));
+    CK(h, launch_split(h->Ap.p, h->Ap.ld, h->Apb.p, h->Aps.p, h->Ap.ld, (int)h->np, (int)h->np, s));
+  }
   if (h->d > 0) {
     CK(h, upload(h->B, B, is_device, s));
     CK(h, upload(h->Bp, B_prime, is_device, s));
@@ -1004,17 +1035,29 @@ int fastpfp_copy_y(fastpfp_handle* h, float* dst, int dst_is_device) {
   return FASTPFP_OK;
 }
 
+int fastpfp_set_y(fastpfp_handle* h, const float* Y, int is_device) {
+  GUARD(h);
+  if (!Y) return FASTPFP_EINVAL;
+  if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
+  cudaStream_t s = h->stream;
+  CK(h, upload(h->Y, Y, is_device, s));
+  CK(h, cudaMemsetAsync(h->flags, 0, sizeof(int), s));
+  CK(h, launch_check_finite(h->Y.p, h->Y.ld, (int)h->yrows, (int)h->m, h->flags, s));
+  return check_flags(h, "Y");
+}
+
 int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   GUARD(h);
   if (!f) return FASTPFP_EINVAL;
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   if (!h->G.p) CK(h, alloc_buf(h->G, (int)h->n, (int)h->np));
+  if (!h->dot_part) CK(h, alloc_arr(h->dot_part, 2 * (size_t)kDotBlocks));
   cudaStream_t s = h->stream;
   if (h->dist) {
     int rc = dist_gemms(h, lambda, h->G.p, h->G.ld, false);
     if (rc) return rc;
     CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, (int)h->n, (int)h->np,
-                      h->scal + 4, s));
+                      h->dot_part, h->scal + 4, s));
     NK(h, h->nccl->AllReduce(h->scal + 4, h->scal + 4, 2, ncclFloat64, ncclSum, h->comm, s));
     double v[2];
     CK(h, cudaMemcpyAsync(v, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1025,7 +1068,7 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   const int N = (int)h->n, NP = (int)h->np;
   int rc = run_products(h, 0.0, h->G.p, h->G.ld, kEpiAxpy, false, 0.0, nullptr);
   if (rc) return rc;
-  CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, N, NP, h->scal, s));
+  CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, N, NP, h->dot_part, h->scal, s));
   double v[2];
   CK(h, cudaMemcpyAsync(v, h->scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(h, cudaStreamSynchronize(s));

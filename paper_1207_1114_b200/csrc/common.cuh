@@ -140,8 +140,10 @@ cudaError_t launch_check_finite(const float* A, int64_t lda, int rows, int cols,
 cudaError_t launch_fill(float* A, int64_t lda, int rows, int cols, float v, cudaStream_t s);
 cudaError_t launch_zero_slack(float* Y, int64_t ldY, int rows, int m, int n, int np,
                               const int* done, cudaStream_t s);
+// objective sums over X∘G and X∘K; part: kDotBlocks x 2 fp64 scratch
+constexpr int kDotBlocks = 592;
 cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t ld, int rows,
-                        int cols, double* out2, cudaStream_t s);
+                        int cols, double* part, double* out2, cudaStream_t s);
 
 // GEMM: C[M x N] = P[M x K] * Q[N x K]^T (+ epilogue). Both operands K-major.
 enum GemmEpi { kEpiPlain = 0, kEpiAxpy = 1, kEpiSplit = 2, kEpiPG = 3, kEpiRowMax = 4 };

@@ -680,24 +680,37 @@ __global__ void zero_slack_kernel(float* Y, int64_t ldY, int rows, int m, int n,
   }
 }
 
-// out2[0] = sum X∘G, out2[1] = sum X∘K  (fp64; single block so the order is fixed)
-__global__ void dot2_kernel(const float* X, const float* G, const float* K, int64_t ld, int rows,
-                            int cols, double* out2) {
+// out2[0] = sum X∘G, out2[1] = sum X∘K (fp64). Grid reduction in a fixed order: block b sums rows
+// b, b + kDotBlocks, ... (lanes stride the columns) into part[2b], part[2b+1]; dot2_finish adds the
+// partials in block order, so the value is reproducible for a given shape.
+__global__ void __launch_bounds__(256) dot2_kernel(const float* X, const float* G, const float* K,
+                                                   int64_t ld, int rows, int cols, double* part) {
   double s0 = 0.0, s1 = 0.0;
-  const int64_t total = (int64_t)rows * cols;
-  for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
-    const int i = (int)(k / cols), j = (int)(k - (k / cols) * cols);
-    const double x = X[(int64_t)i * ld + j];
-    s0 += x * (double)G[(int64_t)i * ld + j];
-    if (K) s1 += x * (double)K[(int64_t)i * ld + j];
+  for (int i = blockIdx.x; i < rows; i += gridDim.x) {
+    const float* x = X + (int64_t)i * ld;
+    const float* g = G + (int64_t)i * ld;
+    const float* k = K ? K + (int64_t)i * ld : nullptr;
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+      const double xv = x[j];
+      s0 += xv * (double)g[j];
+      if (k) s1 += xv * (double)k[j];
+    }
   }
-  __shared__ double r0[32], r1[32];
+  __shared__ double r0[8], r1[8];
   s0 = warp_sum(s0); s1 = warp_sum(s1);
   if ((threadIdx.x & 31) == 0) { r0[threadIdx.x >> 5] = s0; r1[threadIdx.x >> 5] = s1; }
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0.0, b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += r0[w]; b += r1[w]; }
+    for (int w = 0; w < 8; ++w) { a += r0[w]; b += r1[w]; }
+    part[2 * blockIdx.x] = a; part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void dot2_finish(const double* part, int nblk, double* out2) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < nblk; ++q) { a += part[2 * q]; b += part[2 * q + 1]; }
     out2[0] = a; out2[1] = b;
   }
 }
@@ -756,8 +769,10 @@ cudaError_t launch_zero_slack(float* Y, int64_t ldY, int rows, int m, int n, int
 }
 
 cudaError_t launch_dot2(const float* X, const float* G, const float* K, int64_t ld, int rows,
-                        int cols, double* out2, cudaStream_t s) {
-  dot2_kernel<<<1, 1024, 0, s>>>(X, G, K, ld, rows, cols, out2);
+                        int cols, double* part, double* out2, cudaStream_t s) {
+  const int nblk = std::max(1, std::min(rows, kDotBlocks));
+  dot2_kernel<<<nblk, 256, 0, s>>>(X, G, K, ld, rows, cols, part);
+  dot2_finish<<<1, 32, 0, s>>>(part, nblk, out2);
   return cudaGetLastError();
 }
 

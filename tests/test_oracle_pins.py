@@ -486,3 +486,16 @@ def test_dykstra_is_exact_projection_and_closer_than_alternation():
         assert np.allclose(D.sum(0), 1, atol=1e-8) and np.allclose(D.sum(1), 1, atol=1e-8)
         assert np.all(D >= -1e-10)
         assert np.linalg.norm(Y - D) <= np.linalg.norm(Y - A) + 1e-9
+
+
+def test_edge_error_hand_examples():
+    """||A - X A' X^T||_F^2 at a discrete X, values worked by hand.
+    A is the weighted path 0-1-2 (weights 1, 2); A' is the same path with the weights swapped.
+    Identity assignment: entries (0,1), (1,0) differ by 1 and (1,2), (2,1) by 1 -> 4.
+    Reversal 0->2, 1->1, 2->0 maps A' onto A exactly -> 0. Unequal sizes: A = [[0,3],[3,0]],
+    A' = [[0]], row 1 unmatched (-1) -> both off-diagonal 3s are unexplained -> 18."""
+    A = np.array([[0, 1, 0], [1, 0, 2], [0, 2, 0]], float)
+    Ap = np.array([[0, 2, 0], [2, 0, 1], [0, 1, 0]], float)
+    assert O.edge_error(A, Ap, np.array([0, 1, 2])) == 4.0
+    assert O.edge_error(A, Ap, np.array([2, 1, 0])) == 0.0
+    assert O.edge_error(np.array([[0, 3], [3, 0]], float), np.zeros((1, 1)), np.array([0, -1])) == 18.0
