@@ -1,18 +1,27 @@
 #!/usr/bin/env python
 """bench.py — FastPFP outer iterations/s on B200 (BASELINE.json metric), one JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5|c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c5|c2|c4] [--precision P]
 
 A step = one FastPFP outer iteration (Algorithm 1 lines 3-9): GEMM1 (U = A' X^T),
 GEMM2 (Y = A U^T + lambda K), the projection loop (20 sweeps at c5), blend + rescale. The default
 workload is BASELINE.json configs[4] (c5: n = n' = 16384, d = 64, fixed 20 x 20), whose inputs
 (A, A', Y: 1.07 GB each) are larger than the 126 MB L2, so no L2 flush is needed between steps.
-The n = 1000 headline (configs[1], c2) is measured on the same line under "secondary".
+With N > 1 GPUs c5 is row-sharded over the ranks (one pair, strong scaling) and
+`--workload c4` splits BASELINE configs[3]'s 8192 pairs evenly (no communication).
+`python bench.py --gpus N` without a torchrun environment re-launches itself under
+`torch.distributed.run` with N ranks on 127.0.0.1.
 
 Timing: W untimed warm-up steps, then exactly K steps between barrier + cuda.synchronize on both
 sides, timed with CUDA events on the handle's stream (torch's current stream), max over ranks.
 Per-kernel device time (GEMM vs projection) comes from the library's own CUDA events on the same
 stream (FASTPFP_OPT_PROFILE). nvidia-smi clocks are sampled during the timed region.
+
+Roofline bookkeeping: GEMM flops 2nn'(n+n') per outer iteration;
+projection ALGORITHMIC bytes 8 m^2 k (one read + one write of Y per sweep) + 12 n n' (the finalize
+reads X and Y's X block and writes X) — anything else the kernel moves (the sums pass after the
+GEMM, the second finalize pass, X's digit planes) is overhead, visible in `traffic` (ncu DRAM bytes).
 
 --impl reference runs the fp64 CPU oracle (oracle/, the only other place bench.py executes it) on
 a bounded sample of the same workload (rank 0 only) and prints the same JSON line.
@@ -21,20 +30,24 @@ from __future__ import annotations
 
 import argparse
 import json
-
-import numpy as np
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FastPFP outer iters/s at n=1000 & 16384 (1–8 GPU); TFLOP/s & HBM GB/s vs peak"
 UNIT = "outer_iters/s"
+SMS = 148
+# tcgen05 issue rates measured on this part (profiles/r01_tcgen05_peak_micro.txt), MAC/clk/SM
+I8_MAC_CLK, TF32_MAC_CLK = 8192, 2048
 
 
 def load_peaks():
@@ -54,8 +67,9 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, period_ms: int = 50):
         self.idx = device_index
+        self.period = period_ms
         self.proc = None
         self.path = None
 
@@ -65,7 +79,8 @@ class Clocks:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", str(self.period)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.15)          # the first sample lands before the timed region starts
         except Exception:
             self.proc = None
 
@@ -118,7 +133,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dev = "cuda" if (torch.cuda.is_available() and dist.get_backend() == "nccl") else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -129,8 +145,29 @@ def barrier(world):
         dist.barrier()
 
 
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(argv, gpus: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) with torch.distributed.run
+    on 127.0.0.1, the same launch the driver uses; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
+def finish_pg(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------------------------------------
-# workload
+# workload and roofline bookkeeping
 # ------------------------------------------------------------------------------------------------
 def make_problem(workload: str):
     from paper_1207_1114_b200 import inputs
@@ -149,14 +186,16 @@ def workload_desc(p, workload):
             f"eps1=eps2={p.eps1}, I0=I1={p.max_iter1}")
 
 
-def proj_bytes_per_outer(n, npr, sweeps, prec=0, fused_digits=False):
-    """Algorithmic HBM bytes of one projection launch: the sums pass reads Y
-    (4 m^2), each sweep reads + writes Y (8 m^2), the finalize reads X and Y[0:n,0:n'] twice and
-    writes X (4 * 5 n n') plus, for the TF32 GEMMs, X's TF32 split (another 4 * 2 n n'), or on the
-    single-GPU int8 path X's three digit planes (3 n n')."""
+def proj_alg_bytes(n, npr, sweeps):
+    """SURVEY §8(d) algorithmic bytes of the projection + finalize of one outer iteration: each
+    sweep reads and writes Y once (8 m^2), the finalize reads X and Y[0:n,0:n'] and writes X (12 nn')."""
     m = max(n, npr)
-    fin = 28 if prec != 3 else (23 if fused_digits else 20)
-    return 4 * m * m + 8 * m * m * sweeps + fin * n * npr
+    return 8 * m * m * sweeps + 12 * n * npr
+
+
+def step_alg_bytes(n, npr, sweeps, lam_k):
+    """SURVEY §8(d) B_alg per outer iteration: 4 (n^2 + n'^2 + 7 n n' [+ n n' for K]) + 8 m^2 k."""
+    return 4 * (n * n + npr * npr + 7 * n * npr + (n * npr if lam_k else 0)) + 8 * max(n, npr) ** 2 * sweeps
 
 
 def precision_name(prec):
@@ -164,25 +203,36 @@ def precision_name(prec):
 
 
 def gemm_peak(mp, src, prec):
-    """Peak for the GEMM's own dtype: TF32 = measured bf16 x 0.5 (nominal tf32/bf16 ratio,
-    B200_PROFILING.md: 1.1 vs 2.25 PF dense); 3xTF32 issues 3 TF32 MMAs per fp32-accurate product,
-    so its algorithmic-flop peak is a third of that. SIMT fp32: 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
+    """Algorithmic-flop peak of one fp32-accurate product in the GEMM's own dtype (B200_PROFILING.md:
+    another dtype's measured peak x the guide's nominal ratio; the sustained figure for a kernel
+    timed inside a long step). int8 = bf16 x 4.5/2.25, 6 int8 MMAs per product; TF32 = bf16 x
+    1.1/2.25, 3 MMAs per product for 3xTF32. SIMT fp32: 148 SMs x 128 FMA/clk x 2 x 1.965 GHz."""
+    bf = mp["bf16_tflops_sustained"]
     if prec == 2:
-        return 148 * 128 * 2 * 1.965e9 / 1e12, "alu", f"fp32 FFMA peak 74.4 TF/s (148 SMs x 128 lanes x 2 flop x 1.965 GHz, derived)"
+        return SMS * 128 * 2 * 1.965e9 / 1e12, "alu", "fp32 FFMA peak 74.4 TF/s (148 SMs x 128 lanes x 2 flop x 1.965 GHz, derived)"
     if prec == 3:
-        # the GEMM runs inside a long step: sustained figure (B200_PROFILING.md)
-        i8 = mp["bf16_tflops_sustained"] * 2.0
-        return i8 / 6.0, "tensor", (f"int8 Ozaki: ({src} bf16 sustained {mp['bf16_tflops_sustained']} x 4.5/2.25 "
-                                    f"nominal int8/bf16 dense ratio = {i8:.0f} TOPS) / 6 int8 MMAs per "
-                                    f"fp32-accurate product")
-    tf32 = mp["bf16_tflops"] * (1.1 / 2.25)
+        i8 = bf * 4.5 / 2.25
+        return i8 / 6.0, "tensor", (f"int8 Ozaki: ({src} bf16 sustained {bf} x 4.5/2.25 nominal int8/bf16 dense ratio "
+                                    f"= {i8:.0f} TOPS) / 6 int8 MMAs per fp32-accurate product")
+    tf32 = bf * 1.1 / 2.25
     if prec == 1:
-        return tf32, "tensor", f"tf32 = {src} bf16 burst {mp["bf16_tflops"]} x 1.1/2.25 (nominal dense ratio)"
-    return tf32 / 3.0, "tensor", (f"3xTF32: ({src} bf16 burst {mp["bf16_tflops"]} x 1.1/2.25 nominal tf32/bf16 dense ratio) / 3 "
+        return tf32, "tensor", f"tf32 = {src} bf16 sustained {bf} x 1.1/2.25 (nominal dense ratio)"
+    return tf32 / 3.0, "tensor", (f"3xTF32: ({src} bf16 sustained {bf} x 1.1/2.25 nominal tf32/bf16 dense ratio) / 3 "
                                   f"TF32 MMAs per fp32-accurate product")
 
 
+def pipe_peak(prec, sm_mhz):
+    """The same kernel against the tcgen05 issue rate measured on this part at the median SM clock
+    seen during the timed region (algorithmic flops: 6 int8 / 3 TF32 MMAs per fp32-accurate product)."""
+    mac = {3: I8_MAC_CLK / 6.0, 0: TF32_MAC_CLK / 3.0, 1: float(TF32_MAC_CLK)}.get(prec)
+    if not mac or not sm_mhz:
+        return None
+    return SMS * mac * 2 * sm_mhz * 1e6 / 1e12
+
+
 def ncu_traffic(kernel_key):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed ncu
+    --set full capture summarised in profiles/ncu_summary.json."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
@@ -192,8 +242,32 @@ def ncu_traffic(kernel_key):
 
 
 # ------------------------------------------------------------------------------------------------
-# our arm
+# our arm: c5 (default) / c2 on the fixed schedule
 # ------------------------------------------------------------------------------------------------
+def timed_steps(s, p, inner, steps, world, local, stream, clock_ms=50):
+    """Exactly `steps` outer iterations between barrier + synchronize, CUDA events on the stream."""
+    import torch
+    s.reset_stats()
+    barrier(world)
+    torch.cuda.synchronize()
+    clk = Clocks(local, clock_ms)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done = 0
+    while done < steps:
+        k = min(64, steps - done)
+        _, rep = s.iterate(p.alpha, p.lam, 0.0, 0.0, k, inner, want_x=False, trace=0)
+        if rep.iterations == 0 or rep.degenerate:
+            raise SystemExit(f"bench: degenerate iterate after {done} steps (max X~ <= 1e-300)")
+        done += rep.iterations
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    c = clk.stop()
+    return e0.elapsed_time(e1), c, s.stats()
+
+
 def run_ours(args):
     import torch
 
@@ -204,7 +278,6 @@ def run_ours(args):
     torch.cuda.set_device(local)
     maybe_init_pg(world, "nccl")
     mp, src = load_peaks()
-    prec = args.precision
 
     p = make_problem(args.workload)
     inner = p.max_iter2 if args.workload == "c5" else 20
@@ -220,7 +293,9 @@ def run_ours(args):
         A_l, Ap_l, B_l, Bp_l = p.A, p.Ap, p.B, p.Bp
     stream = torch.cuda.current_stream()
     s.set_option(F.OPT_STREAM, stream.cuda_stream)
-    s.set_option(F.OPT_PRECISION, prec)
+    if args.precision is not None:
+        s.set_option(F.OPT_PRECISION, args.precision)
+    prec = s.get_option(F.OPT_PRECISION)        # the library default unless --precision is given
     s.set_option(F.OPT_CHECK_EVERY, 64)
     s.set_graphs(A_l, Ap_l, B_l, Bp_l)
     if p.X0 is not None:
@@ -229,70 +304,42 @@ def run_ours(args):
     # warm-up (untimed)
     s.iterate(p.alpha, p.lam, 0.0, 0.0, max(args.warmup, 1), inner, want_x=False)
     s.set_option(F.OPT_PROFILE, 1)
-
-    def timed():
-        s.reset_stats()
-        barrier(world)
-        torch.cuda.synchronize()
-        clk = Clocks(local)
-        clk.start()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        done = 0
-        while done < args.steps:
-            k = min(64, args.steps - done)
-            _, rep = s.iterate(p.alpha, p.lam, 0.0, 0.0, k, inner, want_x=False, trace=0)
-            done += rep.iterations
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        c = clk.stop()
-        return e0.elapsed_time(e1), c, s.stats()
-
-    ms, clocks, st = timed()
+    ms, clocks, st = timed_steps(s, p, inner, args.steps, world, local, stream)
     if set(clocks.get("reasons", [])) & BAD_REASONS:
-        ms, clocks, st = timed()   # rejected run (thermal / hw slowdown): re-measure once
+        ms, clocks, st = timed_steps(s, p, inner, args.steps, world, local, stream)   # re-measure once
         clocks["remeasured"] = True
     ms_max = max_over_ranks(ms, world)
     # sharded: the ranks cooperate on ONE pair (strong scaling); else every rank runs its own pair
     value = args.steps / (ms_max / 1e3) if sharded else args.steps * world / (ms_max / 1e3)
-
-    # roofline of the dominant kernel (the GEMM at c5; one kernel, two launches per step)
-    gemm_ms = st["gemm_ms"] / max(st["gemm_launches"], 1)
-    flops_launch = st["gemm_flops"] / max(st["gemm_launches"], 1)
-    achieved_tf = flops_launch / (gemm_ms / 1e3) / 1e12
-    peak, bound, peak_note = gemm_peak(mp, src, prec)
-    proj_ms = st["proj_ms"] / max(st["proj_launches"], 1)
-    rows_local = shard.rows if sharded else p.n
-    fused = prec == 3 and not sharded and not st.get("onchip_launches", 0)   # streaming finalize writes X digits
-    pbytes = proj_bytes_per_outer(p.n, p.n_prime, inner, prec, fused_digits=fused) * rows_local // p.n
-    proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
     step_ms = ms / args.steps
-    # the same kernel against the tcgen05 issue rate measured on this part (8192 int8 / 2048 TF32
-    # MAC/clk/SM, profiles/r01_tcgen05_peak_micro.txt) at the clock seen during the timed region
-    mac_clk = {3: 8192 / 6.0, 0: 2048 / 3.0, 1: 2048.0}.get(prec)
-    pipe = None
-    if mac_clk and clocks.get("sm_mhz"):
-        pipe_peak = 148 * mac_clk * 2 * clocks["sm_mhz"] * 1e6 / 1e12
-        pipe = {"peak": round(pipe_peak, 1), "frac": round(achieved_tf / pipe_peak, 4),
-                "source": f"measured tcgen05 issue rate x 148 SMs x median SM clock {clocks['sm_mhz']} MHz"}
-    roofline = {
-        "kernel": f"gemm_{precision_name(prec)}", "bound": bound, "achieved": round(achieved_tf, 2),
-        "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
-        "traffic": ncu_traffic(f"gemm_{precision_name(prec)}") if args.workload == "c5" else None,
-        "flops_per_launch": flops_launch, "ms_per_launch": round(gemm_ms, 4),
-        "share_of_step": round(2 * gemm_ms / step_ms, 4), "peak_source": peak_note,
-        "vs_measured_pipe": pipe,
-        "note": ("gemm_ms spans both GEMM launches and, when sharded, the NCCL all-gather between them"
-                 if sharded else "per GEMM launch (GEMM1 and GEMM2 have equal flops at n = n')"),
-        "secondary": {
-            "kernel": "proj_kernel (sums + 20 sweeps + finalize)", "bound": "hbm",
-            "achieved": round(proj_gbs, 1), "peak": mp["hbm_gbs"], "unit": "GB/s",
-            "frac": round(proj_gbs / mp["hbm_gbs"], 4), "bytes_per_launch": pbytes,
-            "ms_per_launch": round(proj_ms, 4), "share_of_step": round(proj_ms / step_ms, 4),
-            "traffic": ncu_traffic("proj_kernel") if args.workload == "c5" else None,
-            "peak_source": f"{src} hbm_gbs"},
-    }
+    rows_local = shard.rows if sharded else p.n
+
+    roofline = gemm_roofline(mp, src, prec, st, step_ms, clocks, sharded, args.workload == "c5")
+    pbytes = proj_alg_bytes(p.n, p.n_prime, inner) * rows_local // p.n
+    proj_ms = st["proj_ms"] / max(st["proj_launches"], 1)
+    proj_gbs = pbytes / (proj_ms / 1e3) / 1e9
+    roofline["secondary"] = {
+        "kernel": "proj_kernel (sums pass + 20 sweeps + finalize, one launch)" if not sharded else
+                  "projection phase (sums + 20 sweep launches + finalize, NCCL all-reduces between)",
+        "bound": "hbm", "achieved": round(proj_gbs, 1), "peak": mp["hbm_gbs"], "unit": "GB/s",
+        "frac": round(proj_gbs / mp["hbm_gbs"], 4), "bytes_per_launch": pbytes,
+        "bytes_rule": "SURVEY 8(d): 8 m^2 k (sweeps) + 12 n n' (finalize); sums pass, second finalize "
+                      "pass and X digit planes are overhead (in traffic)",
+        "ms_per_launch": round(proj_ms, 4), "share_of_step": round(proj_ms / step_ms, 4),
+        "traffic": ncu_traffic("proj_kernel") if args.workload == "c5" and not sharded else None,
+        "peak_source": f"{src} hbm_gbs (burst copy; the projection runs inside a long step)"}
+    # SURVEY 8(d) composite: T_roof = max(F/peak_tensor, B/BW), T_seq = F/peak + B/BW (per rank)
+    F_step = 2.0 * rows_local * p.n_prime * (p.n + p.n_prime)
+    B_step = step_alg_bytes(p.n, p.n_prime, inner, p.lam != 0 and p.d > 0) * rows_local / p.n
+    t_tensor = F_step / (roofline["peak"] * 1e12) * 1e3
+    t_hbm = B_step / (mp["hbm_gbs"] * 1e9) * 1e3
+    composite = {"flops_per_step": F_step, "alg_bytes_per_step": B_step,
+                 "t_tensor_ms": round(t_tensor, 3), "t_hbm_ms": round(t_hbm, 3),
+                 "t_roof_ms": round(max(t_tensor, t_hbm), 3), "t_seq_ms": round(t_tensor + t_hbm, 3),
+                 "t_step_ms": round(step_ms, 3), "frac_roof": round(max(t_tensor, t_hbm) / step_ms, 4),
+                 "frac_seq": round((t_tensor + t_hbm) / step_ms, 4),
+                 "note": "peaks: roofline.peak (tensor, per fp32-accurate product) and measured hbm_gbs"
+                         + ("; all-gather bytes over NVLink not included" if sharded else "")}
 
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -309,27 +356,52 @@ def run_ours(args):
                                    else ("replicas" if world > 1 else "single")),
                    "l2": "inputs larger than L2 (A, A', Y 1.07 GB each vs 126 MB L2); no flush needed"
                    if args.workload == "c5" else "working set L2-resident"},
-        "roofline": roofline, "clocks": clocks, "gpu_launches": int(st["launches"]),
+        "roofline": roofline, "composite": composite, "clocks": clocks, "gpu_launches": int(st["launches"]),
     }
 
     # end to end through the public API with HOST buffers (pinned): upload graphs, full 20 x 20
     # solve, read X back
     if not args.no_e2e:
         out["e2e"] = e2e(s, p, inner, stream, world, shard)
-    if rank == 0 and world == 1 and args.workload == "c5" and not args.no_secondary:
-        out["secondary"] = secondary_c2(prec)
-        out["secondary_c4"] = secondary_c4()
-        out["secondary_pg"] = secondary_c2(prec, method=1)
-        out["secondary_fastga"] = secondary_ga(prec)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.workload, steps=2)
+    if args.workload == "c5" and not args.no_secondary:
+        out["full_match"] = full_match(s, p, inner, stream, world, shard)
     s.close()
+    if rank == 0 and world == 1 and args.workload == "c5" and not args.no_secondary:
+        out["precision_lines"] = {precision_name(q): precision_line(p, q, inner, min(args.steps, 6), mp, src)
+                                  for q in (0, 1)}
+        out["secondary_c1"] = secondary_pair("c1")
+        out["secondary"] = secondary_pair("c2")
+        out["secondary_c3"] = secondary_pair("c3")
+        out["secondary_c4"] = secondary_c4(mp, src)
+        out["secondary_pg"] = secondary_pair("c2", method=1)
+        out["secondary_fastga"] = secondary_ga()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload, p)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+    finish_pg(world)
+
+
+def gemm_roofline(mp, src, prec, st, step_ms, clocks, sharded, c5):
+    """Roofline of the dominant kernel (the GEMM at c5: one kernel, two launches per step)."""
+    gemm_ms = st["gemm_ms"] / max(st["gemm_launches"], 1)
+    flops_launch = st["gemm_flops"] / max(st["gemm_launches"], 1)
+    achieved_tf = flops_launch / (gemm_ms / 1e3) / 1e12
+    peak, bound, peak_note = gemm_peak(mp, src, prec)
+    pp = pipe_peak(prec, clocks.get("sm_mhz"))
+    return {
+        "kernel": f"gemm_{precision_name(prec)}", "bound": bound, "achieved": round(achieved_tf, 2),
+        "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
+        "traffic": ncu_traffic(f"gemm_{precision_name(prec)}") if c5 and not sharded else None,
+        "flops_per_launch": flops_launch, "ms_per_launch": round(gemm_ms, 4),
+        "share_of_step": round(st["gemm_launches"] * gemm_ms / max(st["outer_iterations"], 1) / step_ms, 4),
+        "peak_source": peak_note,
+        "vs_measured_pipe": None if pp is None else {
+            "peak": round(pp, 1), "frac": round(achieved_tf / pp, 4),
+            "source": f"measured tcgen05 issue rate x {SMS} SMs x median SM clock {clocks.get('sm_mhz')} MHz"},
+        "note": ("gemm_ms spans both GEMM launches and the NCCL all-gather between them" if sharded
+                 else "per GEMM launch (GEMM1 and GEMM2 have equal flops at n = n')"),
+    }
 
 
 def e2e(s, p, inner, stream, world, shard=None):
@@ -368,7 +440,112 @@ def e2e(s, p, inner, stream, world, shard=None):
             "ms_per_solve": round(ms, 3)}
 
 
-def secondary_ga(prec):
+def full_match(s, p, inner, stream, world, shard=None):
+    """north_star's full-match wall time at c5: the whole 20 x 20 solve from X0 plus the greedy
+    discretization (fastpfp_discretize) to a host assignment, inputs resident on the
+    device (SURVEY 8(d) timing windows)."""
+    import torch
+    res = []
+    for _ in range(2):
+        s.set_x0(None if p.X0 is None else np.ascontiguousarray(p.X0[shard.sl if shard else slice(None)]))
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.iterate(p.alpha, p.lam, 0.0, 0.0, p.max_iter1, inner, want_x=False)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        assign = s.discretize()
+        t2 = time.perf_counter()
+        res.append((t2 - t0, t1 - t0, t2 - t1))
+    wall, solve, disc = min(res)
+    return {"wall_ms": round(max_over_ranks(wall * 1e3, world), 2), "solve_ms": round(solve * 1e3, 2),
+            "discretize_ms": round(disc * 1e3, 2), "outer_iterations": p.max_iter1, "inner_sweeps": inner,
+            "planted_recovery": float(np.mean(assign == p.perm)) if p.perm is not None else None,
+            "what": "iterate(20 outer x 20 sweeps from X0) + fastpfp_discretize to a host assignment (wall clock)"}
+
+
+def precision_line(p, prec, inner, steps, mp, src):
+    """The same c5 step with another GEMM precision (north_star: 3xTF32, with plain TF32 reported
+    separately; plain TF32 is NOT fp32-accurate)."""
+    import torch
+
+    import paper_1207_1114_b200 as F
+    s = F.Solver(p.n, p.n_prime, p.d)
+    stream = torch.cuda.current_stream()
+    s.set_option(F.OPT_STREAM, stream.cuda_stream)
+    s.set_option(F.OPT_PRECISION, prec)
+    s.set_option(F.OPT_CHECK_EVERY, 64)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    s.iterate(p.alpha, p.lam, 0.0, 0.0, 3, inner, want_x=False)
+    s.set_option(F.OPT_PROFILE, 1)
+    ms, clocks, st = timed_steps(s, p, inner, steps, 1, torch.cuda.current_device(), stream)
+    s.close()
+    r = gemm_roofline(mp, src, prec, st, ms / steps, clocks, False, True)
+    return {"value": round(steps / (ms / 1e3), 4), "unit": UNIT, "steps": steps, "ms_per_step": round(ms / steps, 3),
+            "gemm": {k: r[k] for k in ("kernel", "achieved", "peak", "frac", "ms_per_launch", "share_of_step",
+                                       "vs_measured_pipe", "peak_source")},
+            "clocks": clocks, "fp32_accurate": prec != 1}
+
+
+def _pair_problem(name):
+    from paper_1207_1114_b200 import inputs
+    return {"c1": inputs.config1, "c2": inputs.config2, "c3": inputs.config3}[name]()
+
+
+PAIR_DESC = {
+    "c1": "c1 (BASELINE configs[0]): n=n'=64, ER p=0.3 U(0,1), exact planted isomorphism, lambda=0, X0=1/n ones, "
+          "alpha=0.5, eps1=eps2=1e-6, I0=I1=100",
+    "c3": "c3 (BASELINE configs[2]): n=800 vs n'=1000 (200 outliers), ER p=0.4, noise N(0,0.05^2), d=16, "
+          "lambda=0.5, alpha=0.5, eps1=eps2=1e-4, I0=I1=300, slack rows persist",
+}
+
+
+def secondary_pair(name, method=0):
+    """One BASELINE pair config solved to convergence (its eps / I caps) plus greedy discretization:
+    outer iters/s of the solve and the full-match wall time (median of 4 runs)."""
+    import torch
+
+    import paper_1207_1114_b200 as F
+    p = _pair_problem(name)
+    s = F.Solver(p.n, p.n_prime, p.d)
+    stream = torch.cuda.current_stream()
+    s.set_option(F.OPT_STREAM, stream.cuda_stream)
+    s.set_option(F.OPT_CHECK_EVERY, 8)
+    s.set_option(F.OPT_METHOD, method)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    s.set_x0(p.X0)
+    res = []
+    for _ in range(4):
+        s.reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = s.iterate(p.alpha, p.lam, p.eps1, p.eps2, p.max_iter1, p.max_iter2, want_x=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solve_ms = e0.elapsed_time(e1)
+        assign = s.discretize()
+        wall = time.perf_counter() - t0
+        res.append((solve_ms, wall, rep))
+    solve_ms, wall, rep = sorted(res, key=lambda r: r[0])[len(res) // 2]
+    acc = float((assign == p.perm).mean())
+    st = s.stats()
+    s.close()
+    desc = PAIR_DESC.get(name) or workload_desc(p, "c2")
+    return {"workload": desc + (" [Projected Gradient {pg}, P:245-249]" if method else ""),
+            "value": round(rep.iterations / (solve_ms / 1e3), 3),
+            "unit": UNIT, "outer_iterations": rep.iterations, "total_sweeps": rep.total_sweeps,
+            "converged": rep.converged,
+            "solve_ms": round(solve_ms, 3), "full_match_wall_ms": round(wall * 1e3, 3),
+            "planted_recovery": acc, "ms_per_sweep": round(solve_ms / max(rep.total_sweeps, 1), 5),
+            "bound": "latency (L2/on-chip resident working set; one grid exchange per sweep)",
+            "proj_kernel": ("on-chip tiles (%d CTAs, 1 grid barrier per sweep)" % st["onchip_tiles"]
+                            if st["onchip_launches"] else "streaming (2 grid barriers per sweep)"),
+            "paper_context": "a few seconds for 1000-node graphs on a 3 GHz Core2 PC in MATLAB (PAPER.md:33-34)"}
+
+
+def secondary_ga():
     """FastGA at n = 1000 on the GA-scaled c2 recipe (inputs.ga_pair):
     full annealing run (beta 0.5 x 1.075^t <= 10, eps = 1e-4, <= 100 Sinkhorn sweeps) + greedy,
     next to FastPFP's c2 solve (the paper's speed comparison)."""
@@ -381,7 +558,6 @@ def secondary_ga(prec):
     s = F.Solver(p.n, p.n_prime, p.d)
     stream = torch.cuda.current_stream()
     s.set_option(F.OPT_STREAM, stream.cuda_stream)
-    s.set_option(F.OPT_PRECISION, prec)
     s.set_option(F.OPT_CHECK_EVERY, 8)
     s.set_option(F.OPT_METHOD, F.METHOD_FASTGA)
     s.set_graphs(p.A, p.Ap, p.B, p.Bp)
@@ -409,141 +585,63 @@ def secondary_ga(prec):
             "planted_recovery": float((assign == p.perm).mean())}
 
 
-def secondary_c2(prec, method=0):
-    """The n = 1000 headline: a full c2 solve to convergence (eps = 1e-4, I = 300/300) plus greedy
-    discretization; reports outer iters/s and full-match wall time."""
-    import torch
-
-    import paper_1207_1114_b200 as F
-    from paper_1207_1114_b200 import inputs
-    p = inputs.config2()
-    s = F.Solver(p.n, p.n_prime, p.d)
-    stream = torch.cuda.current_stream()
-    s.set_option(F.OPT_STREAM, stream.cuda_stream)
-    s.set_option(F.OPT_PRECISION, prec)
-    s.set_option(F.OPT_CHECK_EVERY, 8)
-    s.set_option(F.OPT_METHOD, method)
-    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
-    res = []
-    for rep_i in range(4):
-        s.reset()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        _, rep = s.iterate(p.alpha, p.lam, p.eps1, p.eps2, p.max_iter1, p.max_iter2, want_x=False)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        solve_ms = e0.elapsed_time(e1)
-        assign = s.discretize()
-        wall = time.perf_counter() - t0
-        res.append((solve_ms, wall, rep))
-    solve_ms, wall, rep = sorted(res, key=lambda r: r[0])[len(res) // 2]
-    acc = float((assign == p.perm).mean())
-    st = s.stats()
-    s.close()
-    return {"workload": workload_desc(p, "c2") + (" [Projected Gradient {pg}, P:245-249]" if method else ""),
-            "value": round(rep.iterations / (solve_ms / 1e3), 3),
-            "unit": UNIT, "outer_iterations": rep.iterations, "total_sweeps": rep.total_sweeps,
-            "solve_ms": round(solve_ms, 3), "full_match_wall_ms": round(wall * 1e3, 3),
-            "planted_recovery": acc, "ms_per_sweep": round(solve_ms / max(rep.total_sweeps, 1), 5),
-            "proj_kernel": ("on-chip tiles (%d CTAs, 1 grid barrier per sweep)" % st["onchip_tiles"]
-                            if st["onchip_launches"] else "streaming (2 grid barriers per sweep)"),
-            "paper_context": "a few seconds for 1000-node graphs on a 3 GHz Core2 PC in MATLAB (PAPER.md:33-34)"}
+C4_N = 128
+C4_BATCH = 8192
 
 
-def secondary_c4(batch=8192):
+def c4_roofline(mp, src, pairs, steps, ms, clocks):
+    """The batched kernel's products run on the int8 tensor cores (6 MMAs per fp32-accurate product):
+    4 n^3 algorithmic flops per pair-iteration against the same derived int8 peak as the c5 GEMM."""
+    gflop = 4.0 * C4_N**3 * pairs * steps / 1e9
+    achieved = gflop / (ms / 1e3) / 1e3
+    peak, _, note = gemm_peak(mp, src, 3)
+    pp = pipe_peak(3, clocks.get("sm_mhz"))
+    return {"kernel": "small_solve_tc_kernel (one pair per CTA: products on tcgen05 kind::i8 + sweeps on chip)",
+            "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic("small_solve_tc_kernel"),
+            "flops_rule": "4 n^3 per pair-iteration (the two products of P:387), n = 128",
+            "peak_source": note,
+            "vs_measured_pipe": None if pp is None else {"peak": round(pp, 1), "frac": round(achieved / pp, 4)},
+            "note": "the 20 on-chip sweeps per outer iteration (P:388-391) are not counted as work here; "
+                    "they are what bounds the kernel (DESIGN.md §8)"}
+
+
+def secondary_c4(mp, src, solves=12):
     """BASELINE configs[3]: 8192 pairs of n = 128, fixed 20 outer x 20 sweeps (eps = 0), one pair per
-    CTA (batched whole-solve kernel). Reports pair-outer-iterations/s of one full batch solve."""
+    CTA (batched whole-solve kernel). `solves` back-to-back batch solves in one timed region (enough
+    for >= 10 clock samples)."""
     import torch
 
     import paper_1207_1114_b200 as F
     from paper_1207_1114_b200 import inputs
-    probs = inputs.config4(batch=batch)
+    probs = inputs.config4(batch=C4_BATCH)
     A, Ap, _, _ = inputs.stack_pairs(probs)
-    s = F.BatchedSolver(batch, 128, 128, 0)
+    s = F.BatchedSolver(C4_BATCH, C4_N, C4_N, 0)
     stream = torch.cuda.current_stream()
     s.set_option(F.OPT_STREAM, stream.cuda_stream)
     s.set_graphs(A, Ap)
-    s.iterate(0.5, 0.0, 0.0, 0.0, 2, 20, want_x=False)          # warm-up
-    times = []
-    for _ in range(3):
+    s.iterate(0.5, 0.0, 0.0, 0.0, 3, 20, want_x=False)          # warm-up
+    torch.cuda.synchronize()
+    clk = Clocks(torch.cuda.current_device(), 25)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(solves):
         s.set_x0(None)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
         _, rep = s.iterate(0.5, 0.0, 0.0, 0.0, 20, 20, want_x=False)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = statistics.median(times)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
     assign = s.discretize()
-    acc = float(np.mean([np.array_equal(assign[k], probs[k].perm) for k in range(batch)]))
+    acc = float(np.mean([np.array_equal(assign[k], probs[k].perm) for k in range(C4_BATCH)]))
     s.close()
-    return {"workload": f"c4 (BASELINE configs[3]): {batch} pairs n=n'=128, ER p=0.3, noise N(0,0.02^2), "
+    return {"workload": f"c4 (BASELINE configs[3]): {C4_BATCH} pairs n=n'=128, ER p=0.3, noise N(0,0.02^2), "
                         f"lambda=0, fixed 20 outer x 20 sweeps, one pair per CTA",
-            "value": round(batch * 20 / (ms / 1e3), 1), "unit": "pair_outer_iters/s",
-            "solve_ms": round(ms, 3), "sweeps_per_pair": int(rep.sweeps[0]),
-            "planted_recovery_pairs": acc}
-
-
-# ------------------------------------------------------------------------------------------------
-# the oracle, timed (cpu_baseline and --impl reference)
-# ------------------------------------------------------------------------------------------------
-def oracle_sample(workload, steps):
-    """Time `steps` oracle outer iterations on a bounded sample of the workload and scale to it.
-    c5: the c5 recipe at n = 4096 (20 sweeps per outer), scaled to n = 16384 by n^3 for the two
-    products and n^2 for the projection and blend (Algorithm 1 costs)."""
-    import numpy as np
-
-    from oracle import fastpfp as O
-    from paper_1207_1114_b200 import inputs
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
-    if workload == "c4":   # one outer iteration of 64 of the 8192 pairs, scaled to the batch
-        probs = inputs.config4(first=0, count=64)
-        states = [O.FastPFP(q.A, q.Ap) for q in probs]
-        per_step = []
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            for st in states:
-                st.iterate(0.0, 0.5, 0.0, 0.0, 1, 20)
-            per_step.append((time.perf_counter() - t0) * 8192 / 64)
-        return per_step, cores, f"{steps} oracle outer iteration(s) of 64 c4 pairs (20 sweeps), scaled to 8192 pairs"
-    if workload == "c5":
-        ns = 4096
-        p = inputs.config5(n=ns)
-        scale_n = 16384 / ns
-    else:
-        p = inputs.config2()
-        scale_n = 1.0
-    st = O.FastPFP(p.A, p.Ap, p.B, p.Bp, p.X0)
-    inner = p.max_iter2 if workload == "c5" else 20
-    per_step = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        G = O.gradient(st.A, st.Ap, st.K, st.X, p.lam)
-        t1 = time.perf_counter()
-        st.Y[:p.n, :p.n_prime] = G
-        st.Y, sweeps, delta = O.project_loop(st.Y, 0.0, inner)
-        Xt = (1 - p.alpha) * st.X + p.alpha * st.Y[:p.n, :p.n_prime]
-        st.X = Xt / Xt.max()
-        t2 = time.perf_counter()
-        per_step.append((t1 - t0) * scale_n**3 + (t2 - t1) * scale_n**2)
-    sample = (f"{steps} oracle outer iteration(s) of the {workload} recipe at n={p.n} ({inner} sweeps each), "
-              f"scaled to n={int(p.n * scale_n)} by n^3 (products) and n^2 (projection)") if scale_n != 1 else \
-             f"{steps} oracle outer iteration(s) of {workload} ({inner} sweeps each)"
-    return per_step, cores, sample
-
-
-def cpu_baseline(workload, steps=2):
-    per_step, cores, sample = oracle_sample(workload, steps)
-    t = statistics.median(per_step)
-    return {"value": round(1.0 / t, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": sample, "s_per_outer_scaled": round(t, 3)}
+            "value": round(C4_BATCH * 20 * solves / (ms / 1e3), 1), "unit": "pair_outer_iters/s",
+            "solve_ms": round(ms / solves, 3), "solves_timed": solves, "sweeps_per_pair": int(rep.sweeps[0]),
+            "planted_recovery_pairs": acc, "roofline": c4_roofline(mp, src, C4_BATCH, 20 * solves, ms, clocks),
+            "clocks": clocks}
 
 
 def run_c4(args):
@@ -559,13 +657,13 @@ def run_c4(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     maybe_init_pg(world, "nccl")
-    batch = 8192
-    per = batch // world
+    mp, src = load_peaks()
+    per = C4_BATCH // world
     first = rank * per
-    count = per if rank < world - 1 else batch - first
-    probs = inputs.config4(batch=batch, first=first, count=count)
+    count = per if rank < world - 1 else C4_BATCH - first
+    probs = inputs.config4(batch=C4_BATCH, first=first, count=count)
     A, Ap, _, _ = inputs.stack_pairs(probs)
-    s = F.BatchedSolver(count, 128, 128, 0)
+    s = F.BatchedSolver(count, C4_N, C4_N, 0)
     stream = torch.cuda.current_stream()
     s.set_option(F.OPT_STREAM, stream.cuda_stream)
     s.set_graphs(A, Ap)
@@ -573,7 +671,7 @@ def run_c4(args):
     s.set_x0(None)
     barrier(world)
     torch.cuda.synchronize()
-    clk = Clocks(local)
+    clk = Clocks(local, 25)
     clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -582,33 +680,76 @@ def run_c4(args):
     torch.cuda.synchronize()
     barrier(world)
     clocks = clk.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    ms_local = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms_local, world)
     st = s.stats()
-    # the pair's two n^3 products run on the FP32 pipe (SIMT FFMA): 4 n^3 flop per pair-iteration
-    gflop = 4.0 * 128**3 * batch * args.steps / 1e9
-    achieved = gflop / (ms / 1e3) / 1e3
-    peak = 148 * 128 * 2 * 1.965e9 / 1e12 * world
     assign = s.discretize()
     acc = float(np.mean(np.all(assign == np.stack([p.perm for p in probs]), axis=1)))
-    out = {"metric": METRIC, "value": round(batch * args.steps / (ms / 1e3), 1), "unit": "pair_outer_iters/s",
+    out = {"metric": METRIC, "value": round(C4_BATCH * args.steps / (ms / 1e3), 1), "unit": "pair_outer_iters/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": "c4 (BASELINE configs[3]): 8192 pairs n=n'=128, ER p=0.3, noise N(0,0.02^2), "
                                   "lambda=0, 20 sweeps per outer, one pair per CTA, pairs split evenly over ranks",
                       "parallelism": f"pairs/{world}", "l2": "per-pair working set on chip; inputs 1 GB"},
-           "roofline": {"kernel": "small_solve_kernel", "bound": "alu", "achieved": round(achieved, 2),
-                        "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                        "traffic": None, "note": "GEMM flops only; the 20 on-chip sweeps per outer are latency "
-                                                 "bound (DESIGN.md §8)"},
+           "roofline": c4_roofline(mp, src, count, args.steps, ms_local, clocks),
            "clocks": clocks, "gpu_launches": int(st["launches"]), "planted_recovery_pairs_rank0": acc}
     s.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+    finish_pg(world)
+
+
+# ------------------------------------------------------------------------------------------------
+# the oracle, timed (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_state(p):
+    from oracle import fastpfp as O
+    return O.FastPFP(p.A, p.Ap, p.B, p.Bp, p.X0)
+
+
+def oracle_outer_sample(st, p, inner, sample_sweeps):
+    """One oracle outer iteration of problem p at its FULL size (Algorithm 1 lines 3-9 with the
+    oracle's own functions), with `sample_sweeps` of the `inner` sweeps actually run and the sweep
+    time scaled to `inner` (every sweep of the fixed schedule is the same O(m^2) work).
+    Returns (seconds per outer iteration, detail)."""
+    from oracle import fastpfp as O
+    t0 = time.perf_counter()
+    G = O.gradient(st.A, st.Ap, st.K, st.X, p.lam)                       # line 3 (two n^3 products)
+    t1 = time.perf_counter()
+    st.Y[:p.n, :p.n_prime] = G
+    del G
+    Y, _, _ = O.project_loop(st.Y, 0.0, sample_sweeps)                  # lines 4-7, sampled
+    t2 = time.perf_counter()
+    Xt = (1 - p.alpha) * st.X + p.alpha * Y[:p.n, :p.n_prime]           # lines 8-9
+    X = Xt / Xt.max()
+    t3 = time.perf_counter()
+    del Y, Xt, X
+    per = (t1 - t0) + (t2 - t1) * inner / sample_sweeps + (t3 - t2)
+    return per, {"products_s": round(t1 - t0, 2), "sweep_s": round((t2 - t1) / sample_sweeps, 2),
+                 "finalize_s": round(t3 - t2, 2)}
+
+
+def cpu_baseline(workload, p):
+    """The fp64 oracle as it stands on the host cores, at the bench's own problem size: c5 one outer
+    iteration at n = 16384 with 2 of the 20 sweeps run (the sweep time scaled by 10); c2 one outer
+    iteration at n = 1000 (all 20 sweeps)."""
+    inner = p.max_iter2 if workload == "c5" else 20
+    sample = 2 if workload == "c5" else inner
+    per, detail = oracle_outer_sample(oracle_state(p), p, inner, sample)
+    return {"value": round(1.0 / per, 6), "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": (f"1 oracle outer iteration of the {workload} workload at its full size (n={p.n}): "
+                       f"the two fp64 products, {sample} of the {inner} projection sweeps (time scaled to "
+                       f"{inner}) and the blend + rescale"),
+            "s_per_outer": round(per, 2), **detail}
 
 
 def reference_config(workload):
@@ -627,19 +768,50 @@ def reference_config(workload):
                             f"lambda={p.lam}, alpha={p.alpha}) on c5's fixed schedule: eps = 0, 20 sweeps per "
                             f"outer"),
                "n": p.n, "n_prime": p.n_prime, "d": p.d, "inner_sweeps": 20}
-    cfg["reference"] = "fp64 numpy oracle (oracle/) on host cores, bounded sample scaled to the workload"
+    cfg["reference"] = "fp64 numpy oracle (oracle/) on host cores, bounded sample of the workload"
     return cfg
 
 
 def run_reference(args):
+    """The oracle timed as the reference arm. c5: each step is one full-size (n = 16384) oracle
+    outer iteration with 1 of its 20 sweeps run (scaled by 20); warm-up steps run one full-size
+    sweep only (the products need no warm-up). c2: full outer iterations (20 sweeps). c4: one outer
+    iteration of 64 of the 8192 pairs, scaled to the batch."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    per_warm, cores, sample = oracle_sample(args.workload, max(args.warmup, 0)) if args.warmup else ([], 0, "")
-    per_step, cores, sample = oracle_sample(args.workload, args.steps)
+    from oracle import fastpfp as O
+    from paper_1207_1114_b200 import inputs
+    cores = blas_threads()
+    per_step = []
+    if args.workload == "c4":
+        probs = inputs.config4(first=0, count=64)
+        states = [O.FastPFP(q.A, q.Ap) for q in probs]
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            for st in states:
+                st.iterate(0.0, 0.5, 0.0, 0.0, 1, 20)
+            if k >= args.warmup:
+                per_step.append((time.perf_counter() - t0) * C4_BATCH / 64)
+        sample = "per step: one oracle outer iteration (20 sweeps) of 64 of the 8192 c4 pairs, scaled to the batch"
+        units, unit = C4_BATCH, "pair_outer_iters/s"
+    else:
+        p = make_problem(args.workload)
+        inner = p.max_iter2 if args.workload == "c5" else 20
+        sweeps = 1 if args.workload == "c5" else inner
+        st = oracle_state(p)
+        if args.workload == "c5":
+            for _ in range(args.warmup):
+                O.sweep(st.Y)
+        else:
+            for _ in range(args.warmup):
+                oracle_outer_sample(st, p, inner, sweeps)
+        for _ in range(args.steps):
+            per_step.append(oracle_outer_sample(st, p, inner, sweeps)[0])
+        sample = (f"per step: one oracle outer iteration of {args.workload} at its full size (n={p.n}): the two fp64 "
+                  f"products, {sweeps} of the {inner} sweeps (time scaled to {inner}), blend + rescale")
+        units, unit = 1, UNIT
     total = sum(per_step)
-    units = 8192 if args.workload == "c4" else 1      # c4: pair-outer-iterations of the batch
-    unit = "pair_outer_iters/s" if args.workload == "c4" else UNIT
     value = units * args.steps / total
     out = {"metric": METRIC, "value": round(value, 6), "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
@@ -650,21 +822,46 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def main():
+# ------------------------------------------------------------------------------------------------
+# launcher self-test (CPU, gloo, no kernels): the multi-rank plumbing the GPU run uses
+# ------------------------------------------------------------------------------------------------
+def run_launcher_selftest(args):
+    world, rank, _ = dist_env()
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group(backend="gloo")
+    barrier(world)
+    t = max_over_ranks(float(rank + 1), world)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "gpus_arg": args.gpus, "max_over_ranks": t}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c4"])
-    ap.add_argument("--precision", type=int, default=int(os.environ.get("FASTPFP_BENCH_PRECISION", "3")))
+    ap.add_argument("--precision", type=int, default=None,
+                    help="GEMM precision (FASTPFP_OPT_PRECISION); default: the library's (int8 Ozaki)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--launcher-selftest", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(argv, args.gpus))
     if args.warmup < 3 and args.impl == "ours":
         print("warning: timing rules require >= 3 warm-up steps", file=sys.stderr)
-    if args.impl == "reference":
+    if args.launcher_selftest:
+        run_launcher_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.workload == "c4":
         run_c4(args)

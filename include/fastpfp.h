@@ -230,6 +230,10 @@ int fastpfp_create_dist(int64_t n, int64_t n_prime, int64_t d, int rank, int wor
 /* Set an option (fastpfp_option). Errors: EINVAL for unknown keys or values. */
 int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value);
 
+/* Read the current value of an option (e.g. the precision the handle chose by default).
+ * Errors: EINVAL for unknown keys or a NULL value pointer. */
+int fastpfp_get_option(fastpfp_handle* h, int key, int64_t* value);
+
 /* Read / clear the handle's counters. */
 int fastpfp_get_stats(fastpfp_handle* h, fastpfp_stats* out);
 int fastpfp_reset_stats(fastpfp_handle* h);

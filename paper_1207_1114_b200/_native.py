@@ -103,6 +103,7 @@ def lib():
         "fastpfp_discretize": (C.c_int, [H, VP]),
         "fastpfp_objective": (C.c_int, [H, D, C.POINTER(D)]),
         "fastpfp_set_option": (C.c_int, [H, C.c_int, I64]),
+        "fastpfp_get_option": (C.c_int, [H, C.c_int, C.POINTER(I64)]),
         "fastpfp_get_stats": (C.c_int, [H, C.POINTER(Stats)]),
         "fastpfp_reset_stats": (C.c_int, [H]),
         "fastpfp_destroy": (None, [H]),
@@ -217,6 +218,11 @@ class Solver:
     # -- calls ------------------------------------------------------------------------------
     def set_option(self, key: int, value: int):
         _check(lib().fastpfp_set_option(self._h, key, int(value)), self._h)
+
+    def get_option(self, key: int) -> int:
+        v = C.c_int64()
+        _check(lib().fastpfp_get_option(self._h, key, C.byref(v)), self._h)
+        return v.value
 
     def set_graphs(self, A, Ap, B=None, Bp=None):
         pa, da, ka = _ptr(A)

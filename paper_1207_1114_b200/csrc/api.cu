@@ -596,6 +596,23 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
   return set_err(h, FASTPFP_EINVAL, "unknown option key %d", key);
 }
 
+int fastpfp_get_option(fastpfp_handle* h, int key, int64_t* value) {
+  GUARD(h);
+  if (!value) return FASTPFP_EINVAL;
+  switch (key) {
+    case FASTPFP_OPT_SLACK_MODE: *value = h->slack_mode; return FASTPFP_OK;
+    case FASTPFP_OPT_PRECISION: *value = h->precision; return FASTPFP_OK;
+    case FASTPFP_OPT_RESCALE: *value = h->rescale; return FASTPFP_OK;
+    case FASTPFP_OPT_STREAM: *value = reinterpret_cast<int64_t>(h->stream); return FASTPFP_OK;
+    case FASTPFP_OPT_CHECK_EVERY: *value = h->check_every; return FASTPFP_OK;
+    case FASTPFP_OPT_PROFILE: *value = h->profile; return FASTPFP_OK;
+    case FASTPFP_OPT_GEMM_CTA_GROUP: *value = h->cta_group; return FASTPFP_OK;
+    case FASTPFP_OPT_PROJ_KERNEL: *value = h->proj_kernel; return FASTPFP_OK;
+    case FASTPFP_OPT_METHOD: *value = h->method; return FASTPFP_OK;
+  }
+  return set_err(h, FASTPFP_EINVAL, "unknown option key %d", key);
+}
+
 int fastpfp_set_ga_schedule(fastpfp_handle* h, double beta0, double rate, double beta_max) {
   GUARD(h);
   if (!(beta0 > 0.0) || !std::isfinite(beta0) || !(rate >= 1.0) || !std::isfinite(rate) ||
