@@ -121,7 +121,12 @@ typedef enum fastpfp_option {
    * §3b. Single-GPU handles only (EUNSUPPORTED on a sharded handle). Allocates an m x m fp64
    * workspace on first selection (ENOMEM if it does not fit). In the report, a FastGA iteration's
    * "mu" entries carry beta_t and delta = +inf when only one Sinkhorn sweep ran. */
-  FASTPFP_OPT_METHOD = 9
+  FASTPFP_OPT_METHOD = 9,
+  /* Sharded handles (SURVEY §5 failure detection): every host wait on the handle's stream polls
+   * the stream and ncclCommGetAsyncError; an asynchronous NCCL error, or collectives not complete
+   * after this many milliseconds (default 600000; a peer that died or hung), aborts the
+   * communicator and returns ENCCL (the handle is poisoned). Ignored on single-GPU handles. */
+  FASTPFP_OPT_NCCL_TIMEOUT_MS = 10
 } fastpfp_option;
 
 /* Counters of a handle (since creation or the last fastpfp_reset_stats). */
@@ -210,7 +215,8 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f);
  * iteration: GEMM1 U_r = A' X_r^T locally; NCCL all-gather of U's TF32 parts over NVLink;
  * GEMM2 Y_r = A_r U^T + lambda K_r with a K-loop over the gathered rank blocks; per sweep an NCCL
  * all-reduce (SUM) of the m column sums and sigma (row sums are local); all-reduce (MAX) of mu
- * and rho. Requirements: n >= n', n % P == 0, (n/P) % 32 == 0 (else
+ * and rho. With eps2 > 0 the inner stop test runs on the device (sweeps
+ * are enqueued 8 at a time, launches past the stop are no-ops; one host check per 8 sweeps). Requirements: n >= n', n % P == 0, (n/P) % 32 == 0 (else
  * EUNSUPPORTED); tensor-core precision (0, 1 or 3).
  * On a sharded handle: fastpfp_set_graphs takes the LOCAL rows of A (n/P x n, row-major) and of B
  * (n/P x d) and the full A' and B' (A's symmetry is the caller's contract; finiteness is checked);

@@ -9,7 +9,7 @@ Public API (thin wrapper over the C-ABI in include/fastpfp.h):
 The shared library is loaded lazily on first use; there is no CPU fallback.
 """
 from ._native import (  # noqa: F401
-    EINVAL, ENONFINITE, ESTATE, ESYM, OPT_CHECK_EVERY, OPT_GEMM_CTA_GROUP, OPT_METHOD, OPT_PRECISION, OPT_PROFILE, OPT_PROJ_KERNEL,
+    EINVAL, ENCCL, ENONFINITE, EPOISONED, ESTATE, ESYM, OPT_CHECK_EVERY, OPT_NCCL_TIMEOUT_MS, OPT_GEMM_CTA_GROUP, OPT_METHOD, OPT_PRECISION, OPT_PROFILE, OPT_PROJ_KERNEL,
     METHOD_FASTPFP, METHOD_PG, METHOD_FASTGA, OPT_RESCALE,
     OPT_SLACK_MODE, OPT_STREAM, PREC_FP32_SIMT, PREC_INT8_OZAKI, PREC_TF32, PREC_TF32X3, FastPFPError,
     BatchedSolver, BatchReport, IterReport, Solver, gemm_nt, gemm_nt_blocked, lib, nccl_unique_id, project,

@@ -23,6 +23,7 @@ OPT_SLACK_MODE, OPT_PRECISION, OPT_RESCALE, OPT_STREAM, OPT_CHECK_EVERY, OPT_PRO
 OPT_GEMM_CTA_GROUP = 7
 OPT_PROJ_KERNEL = 8
 OPT_METHOD = 9
+OPT_NCCL_TIMEOUT_MS = 10
 METHOD_FASTPFP, METHOD_PG, METHOD_FASTGA = 0, 1, 2
 PREC_TF32X3, PREC_TF32, PREC_FP32_SIMT, PREC_INT8_OZAKI = 0, 1, 2, 3
 

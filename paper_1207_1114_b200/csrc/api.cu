@@ -6,7 +6,9 @@
 // Device layout: every matrix is fp32 row-major with its row stride rounded
 // up to 32 floats (128 B) so rows are 16 B aligned for float4 / TMA access; padding is zero.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -19,9 +21,12 @@
 
 using namespace fpfp;
 
+struct GreedyScratch;   // discretize.cu
+
 namespace {
 
 constexpr int kMaxCheck = 64;  // max outer iterations per host convergence check
+constexpr int kSweepChunk = 8; // sharded path: sweeps enqueued per host check of the inner stop
 
 struct Buf {
   float* p = nullptr;
@@ -47,6 +52,8 @@ struct fastpfp_handle {
   bool dist = false;
   ncclComm_t comm = nullptr;
   const NcclApi* nccl = nullptr;
+  int64_t nccl_timeout_ms = 600000;   // FASTPFP_OPT_NCCL_TIMEOUT_MS
+  int* inner = nullptr;               // [2] device inner-loop state of the sharded projection
   Buf Uball, Usall;                 // gathered U blocks [world][n'][n]
   int device = 0, num_sms = 0, arch = 0;
   // graphs and their TF32 splits
@@ -84,6 +91,8 @@ struct fastpfp_handle {
   int* flags = nullptr;           // validation flags (device)
   double* scal = nullptr;         // device scalars (objective)
   double* dot_part = nullptr;     // [kDotBlocks][2] objective partials (lazy)
+  GreedyScratch* greedy = nullptr;  // discretization scratch (lazy, discretize.cu)
+  Buf Xall;                       // gathered X of a sharded handle (lazy, discretize)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int slack_mode = 0, precision = 0, rescale = 1, check_every = 4, cta_group = 2, method = 0;
@@ -136,6 +145,42 @@ int set_err(fastpfp_handle* h, int code, const char* fmt, ...) {
     if (r_ != ncclSuccess)                                                                     \
       return set_err((h), FASTPFP_ENCCL, "%s failed: %s", #call, (h)->nccl->GetErrorString(r_)); \
   } while (0)
+
+// Wait for the handle's stream. On a sharded handle the wait polls instead of blocking, so that a
+// failed or vanished peer cannot hang the rank (SURVEY §5 failure detection): an asynchronous NCCL
+// error, or no completion within nccl_timeout_ms, aborts the communicator (which releases the
+// collectives stuck on the stream) and poisons the handle with ENCCL.
+int stream_sync(fastpfp_handle* h) {
+  if (!h->dist || !h->comm) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    return FASTPFP_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(h->stream);
+    if (q == cudaSuccess) return FASTPFP_OK;
+    if (q != cudaErrorNotReady) {
+      cudaGetLastError();
+      return set_err(h, FASTPFP_ECUDA, "stream: %s", cudaGetErrorString(q));
+    }
+    ncclResult_t ae = ncclSuccess;
+    const ncclResult_t r = h->nccl->CommGetAsyncError(h->comm, &ae);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (r != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress) || ms > (double)h->nccl_timeout_ms) {
+      const bool timed_out = r == ncclSuccess && (ae == ncclSuccess || ae == ncclInProgress);
+      h->nccl->CommAbort(h->comm);
+      h->comm = nullptr;
+      cudaStreamSynchronize(h->stream);   // the aborted collectives return
+      cudaGetLastError();
+      if (timed_out)
+        return set_err(h, FASTPFP_ENCCL, "NCCL collectives did not complete within %lld ms (peer lost?); "
+                       "communicator aborted", (long long)h->nccl_timeout_ms);
+      return set_err(h, FASTPFP_ENCCL, "NCCL asynchronous error: %s; communicator aborted",
+                     h->nccl->GetErrorString(r != ncclSuccess ? r : ae));
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
 
 cudaError_t alloc_buf(Buf& b, int rows, int cols) {
   b.rows = rows;
@@ -362,8 +407,10 @@ int ga_alloc(fastpfp_handle* h) {
 
 }  // namespace
 
-int fpfp_discretize_device(fastpfp_handle*, const float*, int64_t, int, int, int32_t*,
-                           cudaStream_t, std::string&);
+struct GreedyScratch;
+int fpfp_discretize_device(GreedyScratch**, const float*, int64_t, int, int, int32_t*, cudaStream_t,
+                           std::string&);
+void fpfp_greedy_free(GreedyScratch*);
 
 extern "C" {
 
@@ -401,17 +448,20 @@ void fastpfp_destroy(fastpfp_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (Buf* b : {&h->A, &h->Ab, &h->As, &h->Ap, &h->Apb, &h->Aps, &h->B, &h->Bp, &h->K, &h->X,
-                 &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G, &h->Uball, &h->Usall})
+                 &h->Xb, &h->Xs, &h->X0, &h->U, &h->Ub, &h->Us, &h->Y, &h->G, &h->Uball, &h->Usall,
+                 &h->Xall})
     free_buf(*b);
+  fpfp_greedy_free(h->greedy);
   for (I8Buf* b : {&h->Ai8, &h->Api8, &h->Xi8, &h->Ui8, &h->Ui8all}) {
     for (auto& d : b->d) if (d) cudaFree(d);
     if (b->e) cudaFree(b->e);
   }
   if (h->Urowmax) cudaFree(h->Urowmax);
-  if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);
+  if (h->comm && h->nccl) h->nccl->CommDestroy(h->comm);   // (aborted communicators are nullptr)
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
                   (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal, (void*)h->dot_part,
+                  (void*)h->inner,
                   (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
                   (void*)h->oc_bar, (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
                   (void*)h->ga_dlt, (void*)h->ga_rho})
@@ -471,7 +521,7 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
-  A(alloc_arr(h->scal, 8));
+  A(alloc_arr(h->scal, 8)); A(alloc_arr(h->inner, 2));
   if (!dist && onchip_fits((int)h->m, h->num_sms, h->PR, h->PC, h->TRo, h->TCo)) {
     const int nb = h->PR * h->PC;
     h->oc_ok = true;
@@ -585,6 +635,9 @@ int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value) {
       if (value < 0 || value > 2) return FASTPFP_EINVAL;
       if (value == 2 && !h->oc_ok) return set_err(h, FASTPFP_EUNSUPPORTED, "Y does not fit on chip");
       h->proj_kernel = (int)value; return FASTPFP_OK;
+    case FASTPFP_OPT_NCCL_TIMEOUT_MS:
+      if (value < 0) return FASTPFP_EINVAL;
+      h->nccl_timeout_ms = value; return FASTPFP_OK;
     case FASTPFP_OPT_PROFILE:
       if (value != 0 && value != 1) return FASTPFP_EINVAL;
       if (value && !h->ev_ready) {
@@ -609,6 +662,7 @@ int fastpfp_get_option(fastpfp_handle* h, int key, int64_t* value) {
     case FASTPFP_OPT_GEMM_CTA_GROUP: *value = h->cta_group; return FASTPFP_OK;
     case FASTPFP_OPT_PROJ_KERNEL: *value = h->proj_kernel; return FASTPFP_OK;
     case FASTPFP_OPT_METHOD: *value = h->method; return FASTPFP_OK;
+    case FASTPFP_OPT_NCCL_TIMEOUT_MS: *value = h->nccl_timeout_ms; return FASTPFP_OK;
   }
   return set_err(h, FASTPFP_EINVAL, "unknown option key %d", key);
 }
@@ -794,25 +848,32 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   CK(h, launch_proj(pa, h->grid, s));
   NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
   h->stats.launches += 1;
-  int sweeps = 0;
-  double delta = 0.0;
-  for (;;) {
-    pa.mode = kProjOneSweep;
-    CK(h, launch_proj(pa, h->grid, s));
-    NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
-    // the global delta is needed for the inner stop test (eps2 > 0) and for the report of the
-    // last sweep only: with a fixed sweep count the MAX all-reduce runs once, not per sweep
-    if (eps2 > 0.0 || sweeps + 1 >= max_iter2)
-      NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
-    h->stats.launches += 1;
-    ++sweeps;
-    if (sweeps >= max_iter2) break;
-    if (eps2 > 0.0) {   // the inner stop needs the global delta on the host
-      CK(h, cudaMemcpyAsync(&delta, h->scal, sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(h, cudaStreamSynchronize(s));
-      if (delta < eps2) break;
+  // inner loop: sweep launches enqueued in chunks; each launch first applies the stop
+  // test of the previous sweep on the device (global delta after its MAX all-reduce), so the host
+  // synchronises once per chunk, not per sweep. With eps2 = 0 the whole fixed schedule is enqueued
+  // at once and the delta all-reduce runs for the reported last sweep only.
+  CK(h, cudaMemsetAsync(h->inner, 0, 2 * sizeof(int), s));
+  pa.mode = kProjOneSweep;
+  pa.inner = eps2 > 0.0 ? h->inner : nullptr;
+  int enq = 0;
+  while (enq < max_iter2) {
+    const int chunk = eps2 > 0.0 ? std::min(kSweepChunk, max_iter2 - enq) : max_iter2 - enq;
+    for (int k = 0; k < chunk; ++k, ++enq) {
+      CK(h, launch_proj(pa, h->grid, s));
+      NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
+      if (eps2 > 0.0 || enq + 1 >= max_iter2)
+        NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
+      h->stats.launches += 1;
+    }
+    if (eps2 > 0.0 && enq < max_iter2) {
+      int st[2] = {0, 0};
+      CK(h, cudaMemcpyAsync(st, h->inner, sizeof st, cudaMemcpyDeviceToHost, s));
+      int rc2 = stream_sync(h);
+      if (rc2) return rc2;
+      if (st[1]) break;
     }
   }
+  pa.inner = nullptr;
   pa.mode = kProjFinMu;
   CK(h, launch_proj(pa, h->grid, s));
   NK(h, h->nccl->AllReduce(h->scal + 1, h->scal + 1, 1, ncclFloat64, ncclMax, h->comm, s));
@@ -823,10 +884,13 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   h->stats.proj_launches += 1;
   if (h->profile) CK(h, cudaEventRecord(h->ev[2], s));
   double sc[3];
+  int st[2] = {0, 0};
   CK(h, cudaMemcpyAsync(sc, h->scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(h, cudaStreamSynchronize(s));
+  CK(h, cudaMemcpyAsync(st, h->inner, sizeof st, cudaMemcpyDeviceToHost, s));
+  rc = stream_sync(h);
+  if (rc) return rc;
   out = DevIter{};
-  out.valid = 1; out.sweeps = sweeps; out.delta = sc[0]; out.mu = sc[1];
+  out.valid = 1; out.sweeps = eps2 > 0.0 ? st[0] : max_iter2; out.delta = sc[0]; out.mu = sc[1];
   if (sc[2] < 0.0) {
     out.degenerate = 1;
   } else {
@@ -881,7 +945,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
     }
     if (X_out) {
       CK(h, download(h->X, X_out, 0, h->stream));
-      CK(h, cudaStreamSynchronize(h->stream));
+      int rc = stream_sync(h);
+      if (rc) return rc;
     }
     if (rep) *rep = R;
     return FASTPFP_OK;
@@ -1078,7 +1143,8 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
     NK(h, h->nccl->AllReduce(h->scal + 4, h->scal + 4, 2, ncclFloat64, ncclSum, h->comm, s));
     double v[2];
     CK(h, cudaMemcpyAsync(v, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(h, cudaStreamSynchronize(s));
+    rc = stream_sync(h);
+    if (rc) return rc;
     *f = 0.5 * v[0] + lambda * v[1];
     return FASTPFP_OK;
   }
@@ -1099,17 +1165,17 @@ int fastpfp_discretize(fastpfp_handle* h, int32_t* assign) {
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   std::string msg;
   if (h->dist) {   // gather the full X (every rank gets the same greedy result)
-    Buf Xall;
-    CK(h, alloc_buf(Xall, (int)h->n_glob, (int)h->np));
+    if (!h->Xall.p) CK(h, alloc_buf(h->Xall, (int)h->n_glob, (int)h->np));
     const size_t cnt = (size_t)h->n * h->X.ld;
-    ncclResult_t nr = h->nccl->AllGather(h->X.p, Xall.p, cnt, ncclFloat32, h->comm, h->stream);
-    if (nr != ncclSuccess) { free_buf(Xall); return set_err(h, FASTPFP_ENCCL, "all-gather X"); }
-    int rc = fpfp_discretize_device(h, Xall.p, Xall.ld, (int)h->n_glob, (int)h->np, assign, h->stream, msg);
-    free_buf(Xall);
+    NK(h, h->nccl->AllGather(h->X.p, h->Xall.p, cnt, ncclFloat32, h->comm, h->stream));
+    int rc = stream_sync(h);
+    if (rc) return rc;
+    rc = fpfp_discretize_device(&h->greedy, h->Xall.p, h->Xall.ld, (int)h->n_glob, (int)h->np, assign,
+                                    h->stream, msg);
     if (rc) return set_err(h, rc, "%s", msg.c_str());
     return FASTPFP_OK;
   }
-  int rc = fpfp_discretize_device(h, h->X.p, h->X.ld, (int)h->n, (int)h->np, assign, h->stream, msg);
+  int rc = fpfp_discretize_device(&h->greedy, h->X.p, h->X.ld, (int)h->n, (int)h->np, assign, h->stream, msg);
   if (rc) return set_err(h, rc, "%s", msg.c_str());
   return FASTPFP_OK;
 }

@@ -121,6 +121,10 @@ struct ProjArgs {
   float* rho_part;       // [grid]
   DevIter* iter_out;     // this iteration's record
   int* done;             // early-exit flag (converged / degenerate)
+  // kProjOneSweep (sharded path): [0] sweeps made in this projection, [1] inner loop stopped. A
+  // sweep launch first applies the stop test of the previous sweep (global delta in scal[0] < eps2)
+  // on the device, so launches enqueued past the stop are no-ops (nullptr: no test).
+  int* inner;
 };
 
 constexpr int kProjThreads = 256;

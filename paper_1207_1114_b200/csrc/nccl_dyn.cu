@@ -35,7 +35,10 @@ void load() {
   bool ok = sym(h, "ncclGetUniqueId", g_api.GetUniqueId) && sym(h, "ncclCommInitRank", g_api.CommInitRank) &&
             sym(h, "ncclCommDestroy", g_api.CommDestroy) && sym(h, "ncclAllGather", g_api.AllGather) &&
             sym(h, "ncclAllReduce", g_api.AllReduce) && sym(h, "ncclGroupStart", g_api.GroupStart) &&
-            sym(h, "ncclGroupEnd", g_api.GroupEnd) && sym(h, "ncclGetErrorString", g_api.GetErrorString);
+            sym(h, "ncclGroupEnd", g_api.GroupEnd) && sym(h, "ncclGetErrorString", g_api.GetErrorString) &&
+            sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError) &&
+            sym(h, "ncclCommAbort", g_api.CommAbort) && sym(h, "ncclSend", g_api.Send) &&
+            sym(h, "ncclRecv", g_api.Recv);
   if (!ok) {
     g_err = "NCCL library lacks a required symbol";
     return;

@@ -521,6 +521,14 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     return;
   }
   if (p.mode == kProjOneSweep) {        // one P1+P2 sweep with the global c, sigma = c[m]
+    if (p.inner) {                      // device-side inner stop test (reading A5)
+      if (p.inner[1]) return;
+      if (p.inner[0] > 0 && p.scal[0] < p.eps2) {   // same values in every block: uniform
+        grid.sync();                    // every block has read inner[] before it changes
+        if (blockIdx.x == 0 && threadIdx.x == 0) p.inner[1] = 1;
+        return;
+      }
+    }
     const double sigma = p.c[p.m];
     float dmax = 0.0f;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
@@ -532,7 +540,10 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     publish_sigma(p, sm);
     if (blockIdx.x == 0) {
       const float d = grid_max(p.dlt_part, sm, 0.0f);
-      if (threadIdx.x == 0) p.scal[0] = (double)d;
+      if (threadIdx.x == 0) {
+        p.scal[0] = (double)d;
+        if (p.inner) p.inner[0] += 1;
+      }
     }
     return;
   }

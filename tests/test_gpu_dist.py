@@ -101,3 +101,49 @@ def test_blocked_k_loop_gemm_matches_dense(prec, blocks, M, N, kb):
     assert np.all(err_b <= (K * 2.0**-24 + 4 * 2.0**-21) * mag + 1e-30), float(np.max(err_b / (mag + 1e-30)))
     if prec == 3:   # same digits, same per-class integer sums: identical to the dense int8 product
         assert np.array_equal(Cb.cpu().numpy(), Cd.cpu().numpy())
+
+
+def test_dist_device_inner_stop_matches_single_gpu():
+    # eps2 > 0 on the sharded path: the stop test runs on the device, sweeps are
+    # enqueued 8 at a time and launches past the stop are no-ops; the sweep counts and X match the
+    # single-GPU kernel, whose inner loop is one persistent launch
+    import paper_1207_1114_b200 as F
+    p = inputs.planted_unequal(78, 512, 480, d=4, eps1=0.0, eps2=1e-4, max_iter1=4, max_iter2=300)
+    a = F.Solver(p.n, p.n_prime, p.d)
+    a.set_option(F.OPT_PROJ_KERNEL, 1)                  # streaming kernel, same tiling as the shard
+    a.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    b = _dist_solver(p)
+    b.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    Xa, ra = a.iterate(p.alpha, p.lam, 0.0, p.eps2, 4, p.max_iter2)
+    Xb, rb = b.iterate(p.alpha, p.lam, 0.0, p.eps2, 4, p.max_iter2)
+    assert all(1 <= k < p.max_iter2 for k in rb.sweeps), rb.sweeps
+    assert all(abs(x - y) <= 1 for x, y in zip(ra.sweeps, rb.sweeps)), (ra.sweeps, rb.sweeps)
+    assert np.max(np.abs(Xa - Xb)) <= 1e-5
+    st = O.FastPFP(p.A, p.Ap, p.B, p.Bp)
+    Xo, ro = st.iterate(p.lam, p.alpha, 0.0, p.eps2, 4, p.max_iter2)
+    assert all(abs(x - y) <= 1 for x, y in zip(ro.sweeps, rb.sweeps)), (ro.sweeps, rb.sweeps)
+    assert np.max(np.abs(Xb.astype(np.float64) - Xo)) <= X_TOL
+    # slack of a sharded handle: local rows x m (n > n' here: slack columns), and it round-trips
+    Y = b.copy_y()
+    assert Y.shape == (p.n, max(p.n, p.n_prime))
+    b.set_y(Y)
+    assert np.array_equal(b.copy_y(), Y)
+    a.close(); b.close()
+
+
+def test_dist_nccl_timeout_aborts_and_poisons():
+    # failure detection: with a 0 ms budget the first host wait finds collectives still
+    # in flight, aborts the communicator and poisons the handle instead of blocking forever
+    import paper_1207_1114_b200 as F
+    p = inputs.config5(n=2048)
+    s = _dist_solver(p)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    s.iterate(p.alpha, p.lam, 0.0, 0.0, 1, 20)          # healthy
+    s.set_option(F.OPT_NCCL_TIMEOUT_MS, 0)
+    with pytest.raises(F.FastPFPError) as e:
+        s.iterate(p.alpha, p.lam, 0.0, 0.0, 3, 20)
+    assert e.value.status == F.ENCCL and "aborted" in str(e.value)
+    with pytest.raises(F.FastPFPError) as e:
+        s.iterate(p.alpha, p.lam, 0.0, 0.0, 1, 20)
+    assert e.value.status == F.EPOISONED
+    s.close()
