@@ -42,6 +42,7 @@ struct __align__(1024) SmemTC {
   float G[kS][kLdG];          // product staging (row = TMEM lane); during the sweeps it holds
                               // the per-warp column partial sums colp[2][kW][kS] (double buffered)
   float csum[kS];             // combined column sums of the current sweep
+  float rsum[2][kW][kRW];     // row sums of each warp's rows (double buffered)
   float dl[2][kW];
   float red[kW];
   int eP[kS], eA[kS], eW[kS]; // row exponents
@@ -117,17 +118,18 @@ __device__ __forceinline__ void split_rows_smem(const float* src, int rows, int 
 // The digit planes of the new X straight from the Y-tile register layout of the blend (warp w owns
 // rows 16w .. 16w + 15, lane l columns 4l .. 4l + 3): no reload from global memory; the 4 digits of
 // a lane's consecutive columns go to shared memory as one packed word per plane.
-__device__ __forceinline__ void split_tile_smem(const float (&x)[kRW][4], int8_t (*d)[kPlane], int* ex) {
+__device__ __forceinline__ void split_tile_smem(const float2 (&x)[kRW][2], int8_t (*d)[kPlane], int* ex) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < kRW; ++r) {
     const int row = warp * kRW + r;
-    float mx = fmaxf(fmaxf(fabsf(x[r][0]), fabsf(x[r][1])), fmaxf(fabsf(x[r][2]), fabsf(x[r][3])));
+    const float v4[4] = {x[r][0].x, x[r][0].y, x[r][1].x, x[r][1].y};
+    float mx = fmaxf(fmaxf(fabsf(v4[0]), fabsf(v4[1])), fmaxf(fabsf(v4[2]), fabsf(v4[3])));
     mx = warp_max(mx);
     const int e = frexp_exp(mx);
     if (lane == 0) ex[row] = e;
     int w1, w2, w3;
-    digits4(x[r], exp2i(-e), w1, w2, w3);
+    digits4(v4, exp2i(-e), w1, w2, w3);
     const int o = swz(row, 4 * lane);
     *reinterpret_cast<int*>(&d[0][o]) = w1;
     *reinterpret_cast<int*>(&d[1][o]) = w2;
@@ -323,6 +325,43 @@ __device__ __forceinline__ void rows_all8(float (&v)[8]) {
     v[r] = __shfl_sync(F, b1, src);
   }
 }
+// element e (0..3) of a lane's 4 consecutive columns held as two float2 pairs
+__device__ __forceinline__ float& el(float2 (&v)[2], int e) {
+  return (e & 1) ? v[e >> 1].y : v[e >> 1].x;
+}
+
+// 8 row partials per lane -> lanes 4r .. 4r + 3 hold the total of row r in v[0] (the halving
+// exchanges of rows_all8 without the final broadcast; the owners publish through shared memory)
+__device__ __forceinline__ void rows_reduce8(float (&v)[8]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float a[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? v[k] : v[4 + k], keep = hi ? v[4 + k] : v[k];
+      a[k] = keep + __shfl_xor_sync(F, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? a[k] : a[2 + k], keep = hi ? a[2 + k] : a[k];
+      b2[k] = keep + __shfl_xor_sync(F, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = keep + __shfl_xor_sync(F, send, 4);
+  }
+  b1 += __shfl_xor_sync(F, b1, 2);
+  b1 += __shfl_xor_sync(F, b1, 1);
+  v[0] = b1;
+}
+
 __device__ __forceinline__ void rows_allreduce(float (&v)[16]) { rows_allreduce16(v); }
 __device__ __forceinline__ void rows_allreduce(float (&v)[8]) { rows_all8<false>(v); }
 __device__ __forceinline__ void rows_allmax(float (&v)[16]) { rows_allmax16(v); }
@@ -364,25 +403,26 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
     // digit planes of the constant graphs (A' is GEMM1's M side, A is GEMM2's)
     split_rows_smem(Ap, np, np, sm.Pd, sm.eP);
     split_rows_smem(A, n, n, sm.Ad, sm.eA);
-    // Y register tile: rows kRW w + r, cols 4l + e
-    float y[kRW][4];
+    // Y register tile: rows kRW w + r, cols 4l + e, as two float2 pairs (e = 0,1 | 2,3) so the
+    // sweep runs on the packed fp32x2 pipe (FADD2)
+    float2 y[kRW][2];
 #pragma unroll
     for (int r = 0; r < kRW; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = warp * kRW + r, j = 4 * lane + e;
-        y[r][e] = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
+        el(y[r], e) = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
       }
 
     int it = 0, conv = 0, total_sweeps = 0, degen = 0;
     float rho = 0.f;
-    float xr[kRW][4];           // X in the Y-tile layout (kept for the blend and the next digits)
+    float2 xr[kRW][2];          // X in the Y-tile layout (kept for the blend and the next digits)
 #pragma unroll
     for (int r = 0; r < kRW; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = warp * kRW + r, j = 4 * lane + e;
-        xr[r][e] = (i < n && j < np) ? X[(int64_t)i * np + j] : 0.f;
+        el(xr[r], e) = (i < n && j < np) ? X[(int64_t)i * np + j] : 0.f;
       }
     split_tile_smem(xr, sm.Wd, sm.eW);
 #ifdef FPFP_SS_PROF
@@ -457,30 +497,37 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
       for (int r = 0; r < kRW; ++r) {
         const int i = warp * kRW + r;
+        if (kFull) {
+          const float4 g = *reinterpret_cast<const float4*>(&sm.G[i][4 * lane]);
+          y[r][0] = make_float2(g.x, g.y);
+          y[r][1] = make_float2(g.z, g.w);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (i < n && 4 * lane + e < np) y[r][e] = sm.G[i][4 * lane + e];
+          for (int e = 0; e < 4; ++e)
+            if (i < n && 4 * lane + e < np) el(y[r], e) = sm.G[i][4 * lane + e];
+        }
       }
       __syncthreads();   // G is read; the column partials of the sweeps reuse its space
 
       SSP(3);
-      // ---- projection loop (P1 + P2 per sweep), sums of the current Y first (as small_solve.cu)
+      // ---- projection loop (P1 + P2 per sweep), sums of the current Y first. Per sweep: the
+      // update and the sums of its output on the packed fp32x2 pipe; a warp's 8 row sums by a
+      // transposed butterfly, published in shared memory with its column partials; one barrier;
+      // the column partials combined by 4 warps (one thread per column); one barrier.
       int buf = 0;
-      float rs[kRW], cs[4];
-      auto sums = [&](float (&yy)[kRW][4]) {
+      auto sums = [&](const float2 (&yy)[kRW][2]) {
+        float rp[kRW];
+        float2 c01 = make_float2(0.f, 0.f), c23 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int r = 0; r < kRW; ++r) rs[r] = (yy[r][0] + yy[r][1]) + (yy[r][2] + yy[r][3]);
-        rows_allreduce(rs);
-        float4 cv;
-        float* ce = reinterpret_cast<float*>(&cv);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float s = 0.f;
-#pragma unroll
-          for (int r = 0; r < kRW; ++r) s += yy[r][e];
-          ce[e] = s;
+        for (int r = 0; r < kRW; ++r) {
+          const float2 t = __fadd2_rn(yy[r][0], yy[r][1]);
+          rp[r] = t.x + t.y;
+          c01 = __fadd2_rn(c01, yy[r][0]);
+          c23 = __fadd2_rn(c23, yy[r][1]);
         }
-        *reinterpret_cast<float4*>(&colp[buf][warp][4 * lane]) = cv;
+        rows_reduce8(rp);                         // lanes 4r..4r+3 now hold the sum of row r
+        if ((lane & 3) == 0) sm.rsum[buf][warp][lane >> 2] = rp[0];
+        *reinterpret_cast<float4*>(&colp[buf][warp][4 * lane]) = make_float4(c01.x, c01.y, c23.x, c23.y);
       };
       sums(y);
       float dmax = 0.f;
@@ -489,34 +536,45 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       int s = 0;
       float delta = 0.f;
       for (;;) {
-        // the kW warp partials of column t combined once (threads 0..127), then read by every warp
-        if (threadIdx.x < kS) {
-          float c = 0.f;
+        if (threadIdx.x < kS) {   // the kW warp partials of column t (conflict-free rows)
+          float c0 = 0.f, c1 = 0.f;
 #pragma unroll
-          for (int w = 0; w < kW; ++w) c += colp[buf][w][threadIdx.x];
-          sm.csum[threadIdx.x] = c;
+          for (int w = 0; w < kW; w += 2) {
+            c0 += colp[buf][w][threadIdx.x];
+            c1 += colp[buf][w + 1][threadIdx.x];
+          }
+          sm.csum[threadIdx.x] = c0 + c1;
         }
         __syncthreads();
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cs[e] = sm.csum[4 * lane + e];
-        const float sigma = warp_sum((cs[0] + cs[1]) + (cs[2] + cs[3]));
+        const float4 cs4 = *reinterpret_cast<const float4*>(&sm.csum[4 * lane]);
+        const float4 rs_lo = *reinterpret_cast<const float4*>(&sm.rsum[buf][warp][0]);
+        const float4 rs_hi = *reinterpret_cast<const float4*>(&sm.rsum[buf][warp][4]);
+        const float sigma = warp_sum((cs4.x + cs4.y) + (cs4.z + cs4.w));
         const float tconst = (1.0f + sigma * inv_m) * inv_m;
-        float cu[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cu[e] = cs[e] * inv_m;
+        const float2 inv2 = make_float2(-inv_m, -inv_m);
+        const float2 ncu01 = __fmul2_rn(make_float2(cs4.x, cs4.y), inv2);   // -c_j / m
+        const float2 ncu23 = __fmul2_rn(make_float2(cs4.z, cs4.w), inv2);
+        const float rsr[8] = {rs_lo.x, rs_lo.y, rs_lo.z, rs_lo.w, rs_hi.x, rs_hi.y, rs_hi.z, rs_hi.w};
         buf ^= 1;
         dmax = 0.f;
 #pragma unroll
         for (int r = 0; r < kRW; ++r) {
           const int i = warp * kRW + r;
-          const float ti = tconst - rs[r] * inv_m;
+          const float ti = tconst - rsr[r] * inv_m;
+          const float2 t2 = make_float2(ti, ti);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = 4 * lane + e;
-            const float yo = y[r][e];
-            const float z = (kFull || (i < m && j < m)) ? fmaxf((yo + ti) - cu[e], 0.f) : 0.f;  // P1, P2
-            if (kDelta) dmax = fmaxf(dmax, fabsf(z - yo));
-            y[r][e] = z;
+          for (int h = 0; h < 2; ++h) {
+            const float2 yo = y[r][h];
+            float2 z = __fadd2_rn(__fadd2_rn(yo, t2), h ? ncu23 : ncu01);    // P1: (y + t_i) - c_j/m
+            z.x = fmaxf(z.x, 0.f);                                            // P2
+            z.y = fmaxf(z.y, 0.f);
+            if (!kFull) {
+              const int j = 4 * lane + 2 * h;
+              if (!(i < m && j < m)) z.x = 0.f;
+              if (!(i < m && j + 1 < m)) z.y = 0.f;
+            }
+            if (kDelta) dmax = fmaxf(dmax, fmaxf(fabsf(z.x - yo.x), fabsf(z.y - yo.y)));
+            y[r][h] = z;
           }
         }
         sums(y);
@@ -537,16 +595,23 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       SSP(4);
 
       // ---- blend + rescale (lines 8-9) on X (registers), row maxima for the next X digits
-      float xt[kRW][4], rmx[kRW];
+      float2 xt[kRW][2];
+      float rmx[kRW];
+      const float2 a2 = make_float2(p.alpha, p.alpha), b2 = make_float2(1.0f - p.alpha, 1.0f - p.alpha);
 #pragma unroll
       for (int r = 0; r < kRW; ++r) {
         const int i = warp * kRW + r;
         rmx[r] = 0.f;                         // X~ >= 0: 0 is the identity of the max
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = 4 * lane + e;
-          xt[r][e] = (1.0f - p.alpha) * xr[r][e] + p.alpha * y[r][e];
-          if (i < n && j < np) rmx[r] = fmaxf(rmx[r], xt[r][e]);
+        for (int h = 0; h < 2; ++h) {
+          xt[r][h] = __ffma2_rn(a2, y[r][h], __fmul2_rn(b2, xr[r][h]));
+          if (kFull) {
+            rmx[r] = fmaxf(rmx[r], fmaxf(xt[r][h].x, xt[r][h].y));
+          } else {
+            const int j = 4 * lane + 2 * h;
+            if (i < n && j < np) rmx[r] = fmaxf(rmx[r], xt[r][h].x);
+            if (i < n && j + 1 < np) rmx[r] = fmaxf(rmx[r], xt[r][h].y);
+          }
         }
       }
       rows_allmax(rmx);
@@ -563,16 +628,21 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       // X / max X as a product with the reciprocal (<= 1 ulp from the quotient)
       const float inv_scale = p.rescale ? 1.0f / mu : 1.0f;
       float rl = 0.f;
+      const float2 is2 = make_float2(inv_scale, inv_scale);
 #pragma unroll
       for (int r = 0; r < kRW; ++r) {
         const int i = warp * kRW + r;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = 4 * lane + e;
-          if (i < n && j < np) {
-            const float xn = xt[r][e] * inv_scale;
-            rl = fmaxf(rl, fabsf(xn - xr[r][e]));
-            xr[r][e] = xn;
+        for (int h = 0; h < 2; ++h) {
+          const float2 xn = __fmul2_rn(xt[r][h], is2);
+          const int j = 4 * lane + 2 * h;
+          if (kFull || (i < n && j < np)) {
+            rl = fmaxf(rl, fabsf(xn.x - xr[r][h].x));
+            xr[r][h].x = xn.x;
+          }
+          if (kFull || (i < n && j + 1 < np)) {
+            rl = fmaxf(rl, fabsf(xn.y - xr[r][h].y));
+            xr[r][h].y = xn.y;
           }
         }
       }
@@ -586,7 +656,8 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           const int e = frexp_exp(rmx[r] * inv_scale);
           if (lane == 0) sm.eW[row] = e;
           int w1, w2, w3;
-          digits4(xr[r], exp2i(-e), w1, w2, w3);   // columns 4 lane .. 4 lane + 3: packed
+          const float v4[4] = {xr[r][0].x, xr[r][0].y, xr[r][1].x, xr[r][1].y};
+          digits4(v4, exp2i(-e), w1, w2, w3);   // columns 4 lane .. 4 lane + 3: packed
           const int o = swz(row, 4 * lane);
           *reinterpret_cast<int*>(&sm.Wd[0][o]) = w1;
           *reinterpret_cast<int*>(&sm.Wd[1][o]) = w2;
@@ -616,7 +687,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = warp * kRW + r, j = 4 * lane + e;
-        if (i < n && j < np) X[(int64_t)i * np + j] = xr[r][e];
+        if (i < n && j < np) X[(int64_t)i * np + j] = el(xr[r], e);
       }
     if (p.Y) {
 #pragma unroll
@@ -624,7 +695,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int i = warp * kRW + r, j = 4 * lane + e;
-          if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = y[r][e];
+          if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = el(y[r], e);
         }
     }
     if (threadIdx.x == 0) {

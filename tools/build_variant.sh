@@ -1,7 +1,9 @@
 #!/bin/bash
-# build a variant of libfastpfp.so with extra -D flags into build/var_<name>/ (experiments only)
+# build a variant of libfastpfp.so with extra -D flags into varlib/var_<name>/ (experiments only;
+# load it with FASTPFP_LIB=varlib/var_<name>/libfastpfp.so; varlib/ travels to the GPU box, build/ does not)
 name=$1; shift
-out=build/var_$name; mkdir -p $out
+out=varlib/var_$name;   # varlib/ travels to the GPU box (build/ does not)
+ mkdir -p $out
 objs=""
 for f in paper_1207_1114_b200/csrc/*.cu; do
   o=$out/$(basename $f).o
