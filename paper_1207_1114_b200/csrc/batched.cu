@@ -21,6 +21,9 @@ struct fastpfp_batched {
   int32_t *iters = nullptr, *conv = nullptr, *sweeps = nullptr, *degen = nullptr, *assign = nullptr;
   float* rho = nullptr;
   int* flags = nullptr;
+  int8_t* dig = nullptr;   // digit-plane images of A', A, X per pair (int8 path, small_solve_tc.cu)
+  int* dexp = nullptr;     // row exponents of A', A per pair
+  bool dig_ready = false;
   cudaStream_t stream = nullptr;
   bool own_stream = false, graphs_set = false, x0_custom = false, poisoned = false;
   int rescale = 1;
@@ -132,6 +135,20 @@ int bflags(fastpfp_batched* h, const char* what) {
   return FASTPFP_OK;
 }
 
+// digit-plane images of the constant graphs for the tensor-core kernel (allocated on first use)
+int bdigits(fastpfp_batched* h) {
+  if (!h->dig) {
+    BCK(h, balloc(h->dig, (size_t)h->batch * small_tc_digit_bytes_per_pair()));
+    BCK(h, balloc(h->dexp, (size_t)h->batch * small_tc_exp_ints_per_pair()));
+  }
+  SmallArgs a{};
+  a.batch = (int)h->batch; a.n = (int)h->n; a.np = (int)h->np; a.A = h->A; a.Ap = h->Ap;
+  a.dig = h->dig; a.dexp = h->dexp;
+  BCK(h, launch_small_digits_prep(a, (int)std::min<int64_t>(h->batch, 8 * h->num_sms), h->stream));
+  h->dig_ready = true;
+  return FASTPFP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -142,7 +159,8 @@ void fastpfp_batched_destroy(fastpfp_batched* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : {(void*)h->A, (void*)h->Ap, (void*)h->B, (void*)h->Bp, (void*)h->K, (void*)h->X,
                   (void*)h->X0, (void*)h->Y, (void*)h->iters, (void*)h->conv, (void*)h->sweeps,
-                  (void*)h->degen, (void*)h->assign, (void*)h->rho, (void*)h->flags})
+                  (void*)h->degen, (void*)h->assign, (void*)h->rho, (void*)h->flags,
+                  (void*)h->dig, (void*)h->dexp})
     if (p) cudaFree(p);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -200,6 +218,7 @@ int fastpfp_batched_set_option(fastpfp_batched* h, int key, int64_t value) {
   if (key == FASTPFP_OPT_PRECISION) {
     if (value != 2 && value != 3) return berr(h, FASTPFP_EINVAL, "batched precision: 2 (fp32 SIMT) or 3 (int8 Ozaki)");
     h->precision = (int)value;
+    if (value == 3 && h->graphs_set && !h->dig_ready) return bdigits(h);
     return FASTPFP_OK;
   }
   return berr(h, FASTPFP_EINVAL, "option %d not supported by the batched path", key);
@@ -234,6 +253,11 @@ int fastpfp_batched_set_graphs(fastpfp_batched* h, const float* A, const float* 
     batched_affinity_kernel<<<grid_for(h->batch * h->n * h->np), 256, 0, s>>>(h->B, h->Bp, h->K, h->batch,
                                                                               (int)h->n, (int)h->np, (int)h->d);
     BCK(h, cudaGetLastError());
+  }
+  h->dig_ready = false;
+  if (h->precision == 3) {
+    rc = bdigits(h);
+    if (rc) return rc;
   }
   rc = breset(h);
   if (rc) return rc;
@@ -274,9 +298,14 @@ int fastpfp_batched_iterate(fastpfp_batched* h, double alpha, double lambda, dou
   a.alpha = (float)alpha; a.lam = (float)lambda; a.eps1 = (float)eps1; a.eps2 = (float)eps2;
   a.max_iter1 = max_iter1; a.max_iter2 = max_iter2; a.rescale = h->rescale;
   a.iters = h->iters; a.conv = h->conv; a.sweeps = h->sweeps; a.rho = h->rho; a.degen = h->degen;
-  const int grid = (int)std::min<int64_t>(h->batch, h->num_sms);
-  if (h->precision == 3) BCK(h, launch_small_solve_tc(a, grid, h->stream));
-  else BCK(h, launch_small_solve(a, grid, h->stream));
+  a.dig = h->dig; a.dexp = h->dexp;
+  if (h->precision == 3) {   // two pairs per CTA (small_solve_tc.cu)
+    const int grid = (int)std::min<int64_t>((h->batch + 1) / 2, h->num_sms);
+    BCK(h, launch_small_solve_tc(a, grid, h->stream));
+  } else {
+    const int grid = (int)std::min<int64_t>(h->batch, h->num_sms);
+    BCK(h, launch_small_solve(a, grid, h->stream));
+  }
   h->stats.launches += 1;
   cudaStream_t s = h->stream;
   if (iterations) BCK(h, cudaMemcpyAsync(iterations, h->iters, h->batch * 4, cudaMemcpyDeviceToHost, s));

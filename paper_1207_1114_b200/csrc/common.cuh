@@ -184,11 +184,18 @@ struct SmallArgs {
   int32_t* sweeps;  // [batch] total sweeps
   float* rho;       // [batch] last rho
   int32_t* degen;   // [batch]
+  // int8 tensor-core kernel (small_solve_tc.cu): per pair the swizzled digit-plane images of A', A
+  // and the current X ([batch][3][3][128 x 128] int8) and the row exponents of A', A ([batch][2][128])
+  int8_t* dig;
+  int* dexp;
 };
 size_t small_smem_bytes();
 cudaError_t launch_small_solve(const SmallArgs& a, int grid, cudaStream_t s);
 // the same whole solve with the products on the int8 tensor cores (small_solve_tc.cu)
 size_t small_tc_smem_bytes();
+size_t small_tc_digit_bytes_per_pair();
+size_t small_tc_exp_ints_per_pair();
+cudaError_t launch_small_digits_prep(const SmallArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_small_solve_tc(const SmallArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_small_greedy(const float* X, int batch, int n, int np, int32_t* assign, int grid,
                                 cudaStream_t s);
