@@ -84,6 +84,12 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
   } while (!ok);
 }
 
+// X~ = (1 - alpha) X + alpha Y in fp64 (Algorithm 1 line 8): one expression shared by every
+// place that forms it, so the fused and the separate mu passes give identical values
+__device__ __forceinline__ double blend_xt(double a, double b, float x, float y) {
+  return __fma_rn(a, (double)y, b * (double)x);
+}
+
 // One tile pass over rows [rb*TR, ...) x cols [cb*512, ...) of Y.
 //   kSweep = false: sums only (Z = Y), accumulated in fp64 (the fresh GEMM output cancels in the
 //   first correction, reading A2 / DESIGN.md §6).
@@ -91,9 +97,12 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 //   accumulated in fp32 per lane (16 values of a row, <= 64 rows of a column) and in fp64 beyond:
 //   their rounding (<= 2^-18 relative) is far below that of the fp32 storage of Y at the same sweep.
 //   kFull: every column of the tile is inside m (no per-element bounds test).
-template <bool kSweep, bool kFull = false>
+//   kMu (last sweep of a fixed-count inner loop, single GPU): the pass also forms X~ from the fresh
+//   Z of the X block and reduces max X~ (mu, line 9) and the per-row max |X~| of the fused X digits,
+//   which saves the separate mu pass over X and Y[0:n, 0:n'] (finalize_mu).
+template <bool kSweep, bool kFull = false, bool kMu = false>
 __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double sigma, float& dmax,
-                                          ProjSmem& sm, Ring& ring_st) {
+                                          ProjSmem& sm, Ring& ring_st, double* mu_acc = nullptr) {
   const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row0 = rb * p.TR;
@@ -200,6 +209,18 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
       }
       double racc = 0.0;
       float racc_f = 0.0f;
+      // kMu: this row's X segment (issued before the element loop; L2/HBM latency overlaps it)
+      float4 xq[kQ];
+      const bool xrow = kMu && i < p.n;
+      if (kMu) {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int j0 = colbase + q * 128 + lane * 4;
+          xq[q] = (xrow && j0 < p.np) ? __ldcs(reinterpret_cast<const float4*>(p.X + (int64_t)i * p.ldX + j0))
+                                      : make_float4(0, 0, 0, 0);
+        }
+      }
+      double xrmax = 0.0;
 #pragma unroll
       for (int q = 0; q < kQ; ++q) {
         float* ve = reinterpret_cast<float*>(&cur[q]);
@@ -218,6 +239,11 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
             ve[e] = z;
             racc_f += z;
             colf[q][e] += z;
+            if (kMu && xrow && j < p.np) {                          // line 8 on the fresh Z
+              const double xt = blend_xt(p.alpha, 1.0 - p.alpha, reinterpret_cast<const float*>(&xq[q])[e], z);
+              *mu_acc = fmax(*mu_acc, xt);
+              xrmax = fmax(xrmax, fabs(xt));
+            }
           } else {
             const double zz = valid ? (double)y : 0.0;
             racc += zz;
@@ -226,6 +252,10 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
         }
       }
       if (kSweep) racc = (double)racc_f;
+      if (kMu && p.xrowmax) {   // per-row max |X~| of this segment (nonnegative doubles order as bits)
+        const double v = warp_max(xrmax);
+        if (lane == 0 && xrow) atomicMax(p.xrowmax + i, (unsigned long long)__double_as_longlong(v));
+      }
       if (kSweep) {
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
@@ -283,6 +313,14 @@ __device__ __forceinline__ void sweep_tile(const ProjArgs& p, int t, double sigm
   const int cb = t - (t / p.CB) * p.CB;
   if ((cb + 1) * kProjTC <= p.m) tile_pass<true, true>(p, t, sigma, dmax, sm, ring);
   else tile_pass<true, false>(p, t, sigma, dmax, sm, ring);
+}
+// the last sweep with the fused mu pass (tiles with no row of the X block take the plain sweep)
+__device__ __forceinline__ void sweep_tile_mu(const ProjArgs& p, int t, double sigma, float& dmax,
+                                              ProjSmem& sm, Ring& ring, double& mu) {
+  const int rb = t / p.CB, cb = t - rb * p.CB;
+  if (rb * p.TR >= p.n || cb * kProjTC >= p.np) { sweep_tile(p, t, sigma, dmax, sm, ring); return; }
+  if ((cb + 1) * kProjTC <= p.m) tile_pass<true, true, true>(p, t, sigma, dmax, sm, ring, &mu);
+  else tile_pass<true, false, true>(p, t, sigma, dmax, sm, ring, &mu);
 }
 
 // r_i = sum_cb rowpart[cb][i], c_j = sum_rb colpart[rb][j]; one warp per index: lane l sums the
@@ -406,7 +444,7 @@ __device__ __forceinline__ double finalize_mu(const ProjArgs& p) {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           if (j0 + e < p.np) {
-            const double xt = b * (double)xe[e] + a * (double)ye[e];
+            const double xt = blend_xt(a, b, xe[e], ye[e]);
             mu_loc = fmax(mu_loc, xt);
             rmx = fmax(rmx, fabs(xt));
           }
@@ -460,7 +498,7 @@ __device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
         for (int e = 0; e < 4; ++e) {
           float xn = 0.0f;
           if (j0 + e < p.np) {
-            const double xt = b * (double)xe[e] + a * (double)ye[e];
+            const double xt = blend_xt(a, b, xe[e], ye[e]);
             xn = (float)(xt * rcp);
             // fl32(|xn - xo|) directly in fp32: IEEE subtraction rounds the exact difference, the
             // same value the former fp64 difference rounded to fp32 gave (2 conversions fewer)
@@ -585,9 +623,17 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 
   int sweeps = 0;
   float delta = 0.0f;
+  bool mu_fused = false;
+  double mu_loc = -INFINITY;
   for (;;) {
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
+    // the cap's last sweep is known in advance: it also reduces mu (the eps2 stop is not)
+    mu_fused = p.do_finalize && sweeps + 1 >= p.max_iter2;
+    if (mu_fused) {
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile_mu(p, t, sigma, dmax, sm, ring, mu_loc);
+    } else {
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
+    }
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
@@ -609,7 +655,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   }
 
   // ---- Algorithm 1 line 8: X~ = (1 - alpha) X + alpha Y[0:n, 0:n'];  line 9: X = X~ / max X~
-  double mu_loc = block_max(finalize_mu(p), sm, (double)-INFINITY);
+  // (mu and the row maxima come from the last sweep when it was the cap's; else one more pass)
+  if (!mu_fused) mu_loc = finalize_mu(p);
+  mu_loc = block_max(mu_loc, sm, (double)-INFINITY);
   if (threadIdx.x == 0) p.mu_part[blockIdx.x] = mu_loc;
   grid.sync();
   const double mu = grid_max(p.mu_part, sm, (double)-INFINITY);
