@@ -49,6 +49,7 @@ struct SlotSm {
   float colp[2][kPW][kS];     // per-warp column partials of the sweeps (double buffered)
   float csum[kS];             // combined column sums of the current sweep
   float rsum[2][kPW][kPR];    // row sums of each warp's rows (double buffered)
+  float wsig[2][kPW];         // per-warp totals (sigma partials, double buffered)
   float dl[2][kPW];
   float red[kPW];
   float xscale[kS];           // 2^(eX - 14): the X digits' row scales (GEMM1's N side)
@@ -482,8 +483,14 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           c01 = __fadd2_rn(c01, yy[r][0]);
           c23 = __fadd2_rn(c23, yy[r][1]);
         }
+        // the warp's share of sigma = 1^T Y 1: an independent reduction that overlaps the butterfly
+        float ws = 0.f;
+#pragma unroll
+        for (int r = 0; r < kPR; ++r) ws += rp[r];
+        ws = warp_sum(ws);
         rows_reduce16(rp);
         if ((lane & 1) == 0) ss.rsum[buf][sw][lane >> 1] = rp[0];
+        if (lane == 0) ss.wsig[buf][sw] = ws;
         *reinterpret_cast<float4*>(&ss.colp[buf][sw][4 * lane]) = make_float4(c01.x, c01.y, c23.x, c23.y);
       };
       sums(y);
@@ -509,7 +516,9 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           const float4 v = *reinterpret_cast<const float4*>(&ss.rsum[buf][sw][q]);
           rsr[q] = v.x; rsr[q + 1] = v.y; rsr[q + 2] = v.z; rsr[q + 3] = v.w;
         }
-        const float sigma = warp_sum((cs4.x + cs4.y) + (cs4.z + cs4.w));
+        const float4 sg0 = *reinterpret_cast<const float4*>(&ss.wsig[buf][0]);
+        const float4 sg1 = *reinterpret_cast<const float4*>(&ss.wsig[buf][4]);
+        const float sigma = ((sg0.x + sg0.y) + (sg0.z + sg0.w)) + ((sg1.x + sg1.y) + (sg1.z + sg1.w));
         const float tconst = (1.0f + sigma * inv_m) * inv_m;
         const float2 inv2 = make_float2(-inv_m, -inv_m);
         const float2 ncu01 = __fmul2_rn(make_float2(cs4.x, cs4.y), inv2);   // -c_j / m
