@@ -591,19 +591,29 @@ C4_BATCH = 8192
 
 def c4_roofline(mp, src, pairs, steps, ms, clocks):
     """The batched kernel's products run on the int8 tensor cores (6 MMAs per fp32-accurate product):
-    4 n^3 algorithmic flops per pair-iteration against the same derived int8 peak as the c5 GEMM."""
+    4 n^3 algorithmic flops per pair-iteration against the same derived int8 peak as the c5 GEMM.
+    Its sweeps (what bounds it) are reported as `secondary` against the fp32 lanes: per element of a
+    sweep P1 is 2 adds, P2 one max, and the row and column sums of the result 2 adds (5 fp32 ops)."""
     gflop = 4.0 * C4_N**3 * pairs * steps / 1e9
     achieved = gflop / (ms / 1e3) / 1e3
     peak, _, note = gemm_peak(mp, src, 3)
     pp = pipe_peak(3, clocks.get("sm_mhz"))
-    return {"kernel": "small_solve_tc_kernel (one pair per CTA: products on tcgen05 kind::i8 + sweeps on chip)",
+    sweep_ops = 5.0 * C4_N * C4_N * 20 * pairs * steps
+    sweep_tops = sweep_ops / (ms / 1e3) / 1e12
+    mhz = clocks.get("sm_mhz") or 1965.0
+    alu_peak = SMS * 128 * mhz * 1e6 / 1e12
+    return {"kernel": "small_solve_tc_kernel (two pairs per CTA: products on tcgen05 kind::i8 + sweeps on chip)",
             "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic("small_solve_tc_kernel"),
             "flops_rule": "4 n^3 per pair-iteration (the two products of P:387), n = 128",
             "peak_source": note,
             "vs_measured_pipe": None if pp is None else {"peak": round(pp, 1), "frac": round(achieved / pp, 4)},
-            "note": "the 20 on-chip sweeps per outer iteration (P:388-391) are not counted as work here; "
-                    "they are what bounds the kernel (DESIGN.md §8)"}
+            "note": "the 20 on-chip sweeps per outer iteration (P:388-391) are what bounds the kernel (DESIGN.md §8)",
+            "secondary": {"what": "the sweeps: 5 fp32 ops per element (P1 2 adds, P2 1 max, row + column sums 2 adds), "
+                                  "20 sweeps of n^2 per pair-iteration, whole kernel time",
+                          "bound": "alu", "achieved": round(sweep_tops, 2), "unit": "Tops/s",
+                          "peak": round(alu_peak, 1), "frac": round(sweep_tops / alu_peak, 4),
+                          "peak_source": f"148 SMs x 128 fp32 lanes x median SM clock {mhz} MHz"}}
 
 
 def secondary_c4(mp, src, solves=12):

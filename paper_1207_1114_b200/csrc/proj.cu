@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -625,6 +626,11 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   float delta = 0.0f;
   bool mu_fused = false;
   double mu_loc = -INFINITY;
+#ifdef FPFP_PROJ_PROF
+  unsigned long long pt[4] = {0, 0, 0, 0}, tmin = ~0ull, tmax = 0;
+  auto gt = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  unsigned long long tq = gt();
+#endif
   for (;;) {
     float dmax = 0.0f;
     // the cap's last sweep is known in advance: it also reduces mu (the eps2 stop is not)
@@ -636,15 +642,32 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     }
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
+#ifdef FPFP_PROJ_PROF
+    { const unsigned long long t = gt(); pt[0] += t - tq; tmin = min(tmin, t - tq); tmax = max(tmax, t - tq); tq = t; }
+#endif
     grid.sync();
+#ifdef FPFP_PROJ_PROF
+    { const unsigned long long t = gt(); pt[1] += t - tq; tq = t; }
+#endif
     reduce_phase(p, sm);
+#ifdef FPFP_PROJ_PROF
+    { const unsigned long long t = gt(); pt[2] += t - tq; tq = t; }
+#endif
     grid.sync();
     sigma = grid_sigma(p, sm);
     delta = grid_max(p.dlt_part, sm, 0.0f);
+#ifdef FPFP_PROJ_PROF
+    { const unsigned long long t = gt(); pt[3] += t - tq; tq = t; }
+#endif
     ++sweeps;
     if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
   }
 
+#ifdef FPFP_PROJ_PROF
+  if ((blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x == 0)
+    printf("proj-prof block %d: per sweep (ns): tiles %llu [min %llu max %llu]  sync1 %llu  reduce %llu  sync2+scalars %llu\n",
+           blockIdx.x, pt[0] / sweeps, tmin, tmax, pt[1] / sweeps, pt[2] / sweeps, pt[3] / sweeps);
+#endif
   if (!p.do_finalize) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       p.iter_out->valid = 1;
