@@ -87,6 +87,10 @@ struct fastpfp_handle {
   double ga_beta0 = 0.5, ga_rate = 1.075, ga_beta_max = 10.0;  // reading G5 defaults
   DevIter* iters = nullptr;       // [kMaxCheck] device
   DevIter* h_iters = nullptr;     // pinned mirror
+  // pinned host scratch for small device->host reads on a sharded handle: a read into pageable
+  // memory would block inside cudaMemcpyAsync until the stream drains, defeating stream_sync's
+  // NCCL fault polling ([0..7] doubles, [8..9] as two ints)
+  double* hpin = nullptr;
   int* done = nullptr;            // device flag
   int* flags = nullptr;           // validation flags (device)
   double* scal = nullptr;         // device scalars (objective)
@@ -467,6 +471,7 @@ void fastpfp_destroy(fastpfp_handle* h) {
                   (void*)h->ga_dlt, (void*)h->ga_rho})
     if (p) cudaFree(p);
   if (h->h_iters) cudaFreeHost(h->h_iters);
+  if (h->hpin) cudaFreeHost(h->hpin);
   if (h->ev_ready)
     for (auto& e : h->ev) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -535,6 +540,7 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
     }
   }
   A(cudaMallocHost(&h->h_iters, kMaxCheck * sizeof(DevIter)));
+  A(cudaMallocHost(&h->hpin, 16 * sizeof(double)));
   A(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   if (rc == FASTPFP_OK && dist) {
@@ -866,8 +872,8 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
       h->stats.launches += 1;
     }
     if (eps2 > 0.0 && enq < max_iter2) {
-      int st[2] = {0, 0};
-      CK(h, cudaMemcpyAsync(st, h->inner, sizeof st, cudaMemcpyDeviceToHost, s));
+      int* st = reinterpret_cast<int*>(h->hpin + 8);
+      CK(h, cudaMemcpyAsync(st, h->inner, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
       int rc2 = stream_sync(h);
       if (rc2) return rc2;
       if (st[1]) break;
@@ -883,10 +889,10 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   h->stats.launches += 2;
   h->stats.proj_launches += 1;
   if (h->profile) CK(h, cudaEventRecord(h->ev[2], s));
-  double sc[3];
-  int st[2] = {0, 0};
+  double* sc = h->hpin;
+  int* st = reinterpret_cast<int*>(h->hpin + 8);
   CK(h, cudaMemcpyAsync(sc, h->scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(h, cudaMemcpyAsync(st, h->inner, sizeof st, cudaMemcpyDeviceToHost, s));
+  CK(h, cudaMemcpyAsync(st, h->inner, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   rc = stream_sync(h);
   if (rc) return rc;
   out = DevIter{};
@@ -943,10 +949,11 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       h->t += 1;
       if (it.converged) { R.converged = 1; break; }
     }
-    if (X_out) {
-      CK(h, download(h->X, X_out, 0, h->stream));
+    if (X_out) {   // wait with fault polling first: a copy into pageable memory would block
       int rc = stream_sync(h);
       if (rc) return rc;
+      CK(h, download(h->X, X_out, 0, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
     }
     if (rep) *rep = R;
     return FASTPFP_OK;
@@ -1141,7 +1148,7 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
     CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, (int)h->n, (int)h->np,
                       h->dot_part, h->scal + 4, s));
     NK(h, h->nccl->AllReduce(h->scal + 4, h->scal + 4, 2, ncclFloat64, ncclSum, h->comm, s));
-    double v[2];
+    double* v = h->hpin + 4;
     CK(h, cudaMemcpyAsync(v, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     rc = stream_sync(h);
     if (rc) return rc;
