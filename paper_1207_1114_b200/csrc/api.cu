@@ -54,6 +54,7 @@ struct fastpfp_handle {
   const NcclApi* nccl = nullptr;
   int64_t nccl_timeout_ms = 600000;   // FASTPFP_OPT_NCCL_TIMEOUT_MS
   int* inner = nullptr;               // [2] device inner-loop state of the sharded projection
+  unsigned* tile_ctr = nullptr;       // projection tile counter (dynamic schedule)
   Buf Uball, Usall;                 // gathered U blocks [world][n'][n]
   int device = 0, num_sms = 0, arch = 0;
   // graphs and their TF32 splits
@@ -465,7 +466,7 @@ void fastpfp_destroy(fastpfp_handle* h) {
   for (void* p : {(void*)h->rowpart, (void*)h->colpart, (void*)h->r, (void*)h->c,
                   (void*)h->sig_part, (void*)h->mu_part, (void*)h->dlt_part, (void*)h->rho_part,
                   (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal, (void*)h->dot_part,
-                  (void*)h->inner,
+                  (void*)h->inner, (void*)h->tile_ctr,
                   (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
                   (void*)h->oc_bar, (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
                   (void*)h->ga_dlt, (void*)h->ga_rho})
@@ -526,7 +527,7 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
-  A(alloc_arr(h->scal, 8)); A(alloc_arr(h->inner, 2));
+  A(alloc_arr(h->scal, 8)); A(alloc_arr(h->inner, 2)); A(alloc_arr(h->tile_ctr, 1));
   if (!dist && onchip_fits((int)h->m, h->num_sms, h->PR, h->PC, h->TRo, h->TCo)) {
     const int nb = h->PR * h->PC;
     h->oc_ok = true;
@@ -1047,6 +1048,8 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
         pa.ldxd = h->Xi8.ld; pa.xe = h->Xi8.e; pa.xrowmax = h->xrowmax;
         CK(h, cudaMemsetAsync(h->xrowmax, 0, (size_t)N * sizeof(unsigned long long), s));
       }
+      pa.tile_ctr = h->tile_ctr;
+      CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
       CK(h, launch_proj(pa, h->grid, s));
       h->stats.launches += 1;
       h->stats.proj_launches += 1;

@@ -125,6 +125,11 @@ struct ProjArgs {
   // sweep launch first applies the stop test of the previous sweep (global delta in scal[0] < eps2)
   // on the device, so launches enqueued past the stop are no-ops (nullptr: no test).
   int* inner;
+  // kProjFull: tile counter (zeroed before the launch). Tiles of each pass are handed out by an
+  // atomic counter instead of a static round robin, so fast blocks take more tiles and the wait at
+  // the pass's grid barrier shrinks; results do not depend on which block ran a tile (partials are
+  // indexed by tile). nullptr: static schedule.
+  unsigned* tile_ctr;
 };
 
 constexpr int kProjThreads = 256;

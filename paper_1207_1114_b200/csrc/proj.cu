@@ -532,6 +532,28 @@ __device__ __forceinline__ float finalize_apply(const ProjArgs& p, double mu) {
   return rho_loc;
 }
 
+// Tile schedule of one pass (pass index `pass`, counted from the launch): with p.tile_ctr every block
+// fetches tiles from one atomic counter. Each pass costs the counter exactly ntiles + gridDim.x
+// increments (every block's last fetch fails), and passes are separated by grid barriers, so pass
+// `pass` owns the counter range [pass (ntiles + grid), ...) without resetting it.
+template <typename F>
+__device__ __forceinline__ void for_tiles(const ProjArgs& p, int ntiles, unsigned pass, unsigned* s_tile,
+                                          F&& body) {
+  if (!p.tile_ctr) {
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) body(t);
+    return;
+  }
+  const unsigned base = pass * (unsigned)(ntiles + gridDim.x);
+  for (;;) {
+    if (threadIdx.x == 0) *s_tile = atomicAdd(p.tile_ctr, 1u) - base;
+    __syncthreads();
+    const unsigned t = *s_tile;
+    __syncthreads();
+    if (t >= (unsigned)ntiles) break;
+    body((int)t);
+  }
+}
+
 __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   if (*p.done) return;  // an earlier iteration of this launch batch converged (uniform)
   cg::grid_group grid = cg::this_grid();
@@ -613,9 +635,11 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   }
 
   // ------------------------------------------------------------------ single GPU: everything
+  __shared__ unsigned s_tile;
+  unsigned pass = 0;
   if (p.do_sums) {
     // sums of the current Y (fresh GEMM block + retained slack)
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm, ring);
+    for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { tile_pass<false>(p, t, 0.0, dummy, sm, ring); });
     grid.sync();
     reduce_phase(p, sm);
     grid.sync();
@@ -636,9 +660,9 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     // the cap's last sweep is known in advance: it also reduces mu (the eps2 stop is not)
     mu_fused = p.do_finalize && sweeps + 1 >= p.max_iter2;
     if (mu_fused) {
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile_mu(p, t, sigma, dmax, sm, ring, mu_loc);
+      for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile_mu(p, t, sigma, dmax, sm, ring, mu_loc); });
     } else {
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
+      for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile(p, t, sigma, dmax, sm, ring); });
     }
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
