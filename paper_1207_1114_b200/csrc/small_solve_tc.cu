@@ -499,6 +499,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       int s = 0;
       float delta = 0.f;
       for (;;) {
+#ifndef FPFP_SS_PER_LANE_COMBINE   // (the per-lane variant below measured no faster: 7.36 vs 7.5 M)
         if (st < kS) {   // the kPW warp partials of column st (conflict-free rows)
           float c0 = 0.f, c1 = 0.f;
 #pragma unroll
@@ -510,6 +511,21 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         }
         slot_sync(slot);
         const float4 cs4 = *reinterpret_cast<const float4*>(&ss.csum[4 * lane]);
+#else
+        // every lane combines the kPW warp partials of its own 4 columns (8 vector loads, in the
+        // fixed warp order): one slot barrier per sweep instead of two
+        float4 cs4;
+        {
+          float2 c01 = make_float2(0.f, 0.f), c23 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int w = 0; w < kPW; ++w) {
+            const float4 v = *reinterpret_cast<const float4*>(&ss.colp[buf][w][4 * lane]);
+            c01 = __fadd2_rn(c01, make_float2(v.x, v.y));
+            c23 = __fadd2_rn(c23, make_float2(v.z, v.w));
+          }
+          cs4 = make_float4(c01.x, c01.y, c23.x, c23.y);
+        }
+#endif
         float rsr[kPR];
 #pragma unroll
         for (int q = 0; q < kPR; q += 4) {
