@@ -852,6 +852,8 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   const size_t mc = (size_t)h->m + 1;
   ProjArgs pa = dist_proj_args(h, kProjSums, h->method == 1 ? 1.0 : alpha, eps1, eps2);
   if (h->method == 1) pa.rescale = 0;
+  pa.tile_ctr = h->tile_ctr;   // dynamic tile schedule: the counter is reset before each pass launch
+  CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
   CK(h, launch_proj(pa, h->grid, s));
   NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
   h->stats.launches += 1;
@@ -866,6 +868,7 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   while (enq < max_iter2) {
     const int chunk = eps2 > 0.0 ? std::min(kSweepChunk, max_iter2 - enq) : max_iter2 - enq;
     for (int k = 0; k < chunk; ++k, ++enq) {
+      CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
       CK(h, launch_proj(pa, h->grid, s));
       NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
       if (eps2 > 0.0 || enq + 1 >= max_iter2)
@@ -881,6 +884,7 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
     }
   }
   pa.inner = nullptr;
+  pa.tile_ctr = nullptr;       // the finalize phases tile by rows of X (static)
   pa.mode = kProjFinMu;
   CK(h, launch_proj(pa, h->grid, s));
   NK(h, h->nccl->AllReduce(h->scal + 1, h->scal + 1, 1, ncclFloat64, ncclMax, h->comm, s));

@@ -571,10 +571,11 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 #endif
   const int ntiles = p.RB * p.CB;
   float dummy = 0.0f;
+  __shared__ unsigned s_tile;
 
   // ------------------------------------------------------------------ distributed phases
   if (p.mode == kProjSums) {            // sums of the local rows of Y -> c_local, r, sigma_local
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) tile_pass<false>(p, t, 0.0, dummy, sm, ring);
+    for_tiles(p, ntiles, 0u, &s_tile, [&](int t) { tile_pass<false>(p, t, 0.0, dummy, sm, ring); });
     grid.sync();
     reduce_phase(p, sm);
     grid.sync();
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     }
     const double sigma = p.c[p.m];
     float dmax = 0.0f;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) sweep_tile(p, t, sigma, dmax, sm, ring);
+    for_tiles(p, ntiles, 0u, &s_tile, [&](int t) { sweep_tile(p, t, sigma, dmax, sm, ring); });
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
     grid.sync();
@@ -635,7 +636,6 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   }
 
   // ------------------------------------------------------------------ single GPU: everything
-  __shared__ unsigned s_tile;
   unsigned pass = 0;
   if (p.do_sums) {
     // sums of the current Y (fresh GEMM block + retained slack)
