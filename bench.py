@@ -370,6 +370,7 @@ def run_ours(args):
         out["precision_lines"] = {precision_name(q): precision_line(p, q, inner, min(args.steps, 6), mp, src)
                                   for q in (0, 1)}
         out["secondary_c1"] = secondary_pair("c1")
+        out["secondary_c1_batched"] = secondary_c1_batched()
         out["secondary"] = secondary_pair("c2")
         out["secondary_c3"] = secondary_pair("c3")
         out["secondary_c4"] = secondary_c4(mp, src)
@@ -543,6 +544,42 @@ def secondary_pair(name, method=0):
             "proj_kernel": ("on-chip tiles (%d CTAs, 1 grid barrier per sweep)" % st["onchip_tiles"]
                             if st["onchip_launches"] else "streaming (2 grid barriers per sweep)"),
             "paper_context": "a few seconds for 1000-node graphs on a 3 GHz Core2 PC in MATLAB (PAPER.md:33-34)"}
+
+
+def secondary_c1_batched():
+    """BASELINE configs[0] through the batched small-pair kernel as a batch of one (the whole solve
+    in one CTA slot: products on the int8 tensor cores, sweeps in registers) — the
+    path a caller with many or tiny pairs uses; the same problem, eps and caps as secondary_c1."""
+    import torch
+
+    import paper_1207_1114_b200 as F
+    from paper_1207_1114_b200 import inputs
+    p = inputs.config1()
+    s = F.BatchedSolver(1, p.n, p.n_prime, 0)
+    stream = torch.cuda.current_stream()
+    s.set_option(F.OPT_STREAM, stream.cuda_stream)
+    s.set_graphs(p.A[None], p.Ap[None])
+    res = []
+    for _ in range(4):
+        s.set_x0(p.X0[None])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = s.iterate(p.alpha, p.lam, p.eps1, p.eps2, p.max_iter1, p.max_iter2, want_x=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solve_ms = e0.elapsed_time(e1)
+        assign = s.discretize()
+        res.append((solve_ms, (time.perf_counter() - t0) * 1e3, rep))
+    solve_ms, wall_ms, rep = sorted(res, key=lambda r: r[0])[len(res) // 2]
+    s.close()
+    iters, sweeps = int(rep.iterations[0]), int(rep.sweeps[0])
+    return {"workload": PAIR_DESC["c1"] + " [batched small-pair kernel, batch of one]",
+            "value": round(iters / (solve_ms / 1e3), 3), "unit": UNIT, "outer_iterations": iters,
+            "total_sweeps": sweeps, "converged": bool(rep.converged[0]), "solve_ms": round(solve_ms, 3),
+            "full_match_wall_ms": round(wall_ms, 3), "planted_recovery": float(np.mean(assign[0] == p.perm)),
+            "ms_per_sweep": round(solve_ms / max(sweeps, 1), 5)}
 
 
 def secondary_ga():

@@ -223,12 +223,15 @@ cudaError_t download(const Buf& b, float* dst, int is_device, cudaStream_t s) {
 }
 
 // projection tiling: largest TR in {512, ..., 8} giving >= 2 tiles per SM, else 8
+#ifndef FPFP_PROJ_MIN_TILES
+#define FPFP_PROJ_MIN_TILES 2   // tiles per SM the row-block height TR must at least give
+#endif
 void plan_projection(fastpfp_handle* h) {
   const int64_t m = h->m, rows = h->yrows;
   const int CB = (int)ceil_div(m, kProjTC);
   int TR = 8;
   for (int tr : {512, 256, 128, 64, 32, 16, 8}) {
-    if (ceil_div(rows, tr) * CB >= 2LL * h->num_sms) { TR = tr; break; }
+    if (ceil_div(rows, tr) * CB >= (int64_t)FPFP_PROJ_MIN_TILES * h->num_sms) { TR = tr; break; }
   }
   h->TR = TR;
   h->CB = CB;
