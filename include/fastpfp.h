@@ -233,6 +233,14 @@ int fastpfp_nccl_unique_id(void* out, int64_t size);
 int fastpfp_create_dist(int64_t n, int64_t n_prime, int64_t d, int rank, int world,
                         const void* nccl_id, fastpfp_handle** out);
 
+/* The collectives the last fastpfp_iterate / fastpfp_objective / fastpfp_discretize call of a
+ * sharded handle issued, in order (empty on single-GPU handles): out[4k .. 4k+3] = {kind (0
+ * all-reduce, 1 all-gather), ncclDataType_t, ncclRedOp_t (-1 for all-gather), element count}; at
+ * most `capacity` entries are written, *count receives the total. The per-outer-iteration sequence
+ * is the one paper_1207_1114_b200/dist.py collective_schedule describes.
+ * Errors: EINVAL. */
+int fastpfp_dist_collectives(fastpfp_handle* h, int64_t* out, int64_t capacity, int64_t* count);
+
 /* Set an option (fastpfp_option). Errors: EINVAL for unknown keys or values. */
 int fastpfp_set_option(fastpfp_handle* h, int key, int64_t value);
 

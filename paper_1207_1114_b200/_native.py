@@ -105,6 +105,7 @@ def lib():
         "fastpfp_objective": (C.c_int, [H, D, C.POINTER(D)]),
         "fastpfp_set_option": (C.c_int, [H, C.c_int, I64]),
         "fastpfp_get_option": (C.c_int, [H, C.c_int, C.POINTER(I64)]),
+        "fastpfp_dist_collectives": (C.c_int, [H, VP, I64, C.POINTER(I64)]),
         "fastpfp_get_stats": (C.c_int, [H, C.POINTER(Stats)]),
         "fastpfp_reset_stats": (C.c_int, [H]),
         "fastpfp_destroy": (None, [H]),
@@ -297,6 +298,14 @@ class Solver:
         self._check_shape(Y, self._y_shape())
         p, dev, keep = _ptr(Y)
         _check(lib().fastpfp_set_y(self._h, p, dev), self._h)
+
+    def collectives(self):
+        """[(kind, nccl dtype, nccl op, count)] issued by the last call of a sharded handle."""
+        cnt = C.c_int64()
+        _check(lib().fastpfp_dist_collectives(self._h, None, 0, C.byref(cnt)), self._h)
+        buf = np.zeros((max(cnt.value, 1), 4), np.int64)
+        _check(lib().fastpfp_dist_collectives(self._h, buf.ctypes.data, cnt.value, C.byref(cnt)), self._h)
+        return [tuple(int(x) for x in row) for row in buf[:cnt.value]]
 
     def stats(self) -> dict:
         st = Stats()

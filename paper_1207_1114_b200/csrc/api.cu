@@ -6,6 +6,7 @@
 // Device layout: every matrix is fp32 row-major with its row stride rounded
 // up to 32 floats (128 B) so rows are 16 B aligned for float4 / TMA access; padding is zero.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <thread>
@@ -55,6 +56,9 @@ struct fastpfp_handle {
   int64_t nccl_timeout_ms = 600000;   // FASTPFP_OPT_NCCL_TIMEOUT_MS
   int* inner = nullptr;               // [2] device inner-loop state of the sharded projection
   unsigned* tile_ctr = nullptr;       // projection tile counter (dynamic schedule)
+  // collectives issued by the last iterate / objective / discretize call of a sharded handle, in
+  // order: {kind (0 all-reduce, 1 all-gather), ncclDataType_t, ncclRedOp_t (-1), count}
+  std::vector<std::array<int64_t, 4>> coll_log;
   Buf Uball, Usall;                 // gathered U blocks [world][n'][n]
   int device = 0, num_sms = 0, arch = 0;
   // graphs and their TF32 splits
@@ -150,6 +154,19 @@ int set_err(fastpfp_handle* h, int code, const char* fmt, ...) {
     if (r_ != ncclSuccess)                                                                     \
       return set_err((h), FASTPFP_ENCCL, "%s failed: %s", #call, (h)->nccl->GetErrorString(r_)); \
   } while (0)
+
+// The sharded path's collectives, logged in issue order (fastpfp_dist_collectives; the schedule the
+// gloo decomposition test follows, paper_1207_1114_b200/dist.py collective_schedule).
+ncclResult_t coll_allreduce(fastpfp_handle* h, void* buf, size_t count, ncclDataType_t t, ncclRedOp_t op,
+                            cudaStream_t s) {
+  h->coll_log.push_back({0, (int64_t)t, (int64_t)op, (int64_t)count});
+  return h->nccl->AllReduce(buf, buf, count, t, op, h->comm, s);
+}
+ncclResult_t coll_allgather(fastpfp_handle* h, const void* send, void* recv, size_t count, ncclDataType_t t,
+                            cudaStream_t s) {
+  h->coll_log.push_back({1, (int64_t)t, -1, (int64_t)count});
+  return h->nccl->AllGather(send, recv, count, t, h->comm, s);
+}
 
 // Wait for the handle's stream. On a sharded handle the wait polls instead of blocking, so that a
 // failed or vanished peer cannot hang the rank (SURVEY §5 failure detection): an asynchronous NCCL
@@ -775,13 +792,13 @@ static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo,
     CK(h, launch_gemm_i8(g1, s, h->device));
     // ... the row scales of U are global: MAX over ranks of the |max| bits (nonneg floats order
     // as unsigned), so every rank splits its block with the same exponents ...
-    NK(h, h->nccl->AllReduce(h->Urowmax, h->Urowmax, (size_t)NP, ncclUint32, ncclMax, h->comm, s));
+    NK(h, coll_allreduce(h, h->Urowmax, (size_t)NP, ncclUint32, ncclMax, s));
     CK(h, split_i8(h->U, h->Ui8, h->Urowmax, nullptr, s));
     // ... all-gather of the 3 digit planes (3 bytes per element instead of 8 for the TF32 parts)
     const size_t cnt = (size_t)NP * h->Ui8.ld;
     NK(h, h->nccl->GroupStart());
     for (int k = 0; k < 3; ++k)
-      NK(h, h->nccl->AllGather(h->Ui8.d[k], h->Ui8all.d[k], cnt, ncclInt8, h->comm, s));
+      NK(h, coll_allgather(h, h->Ui8.d[k], h->Ui8all.d[k], cnt, ncclInt8, s));
     NK(h, h->nccl->GroupEnd());
     // Y_r[:, 0:n'] = A_r U^T + lambda K_r, K-loop over the gathered rank blocks (3-D TMA)
     I8Gemm g2{};
@@ -809,8 +826,8 @@ static int dist_gemms(fastpfp_handle* h, double lambda, float* out, int64_t ldo,
   if (rc) return rc;
   const size_t cnt = (size_t)NP * h->Ub.ld;
   NK(h, h->nccl->GroupStart());
-  NK(h, h->nccl->AllGather(h->Ub.p, h->Uball.p, cnt, ncclFloat32, h->comm, s));
-  NK(h, h->nccl->AllGather(h->Us.p, h->Usall.p, cnt, ncclFloat32, h->comm, s));
+  NK(h, coll_allgather(h, h->Ub.p, h->Uball.p, cnt, ncclFloat32, s));
+  NK(h, coll_allgather(h, h->Us.p, h->Usall.p, cnt, ncclFloat32, s));
   NK(h, h->nccl->GroupEnd());
   // Y_r[:, 0:n'] = A_r U^T + lambda K_r, K-loop over the gathered rank blocks
   GemmArgs g2{};
@@ -858,7 +875,7 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   pa.tile_ctr = h->tile_ctr;   // dynamic tile schedule: the counter is reset before each pass launch
   CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
   CK(h, launch_proj(pa, h->grid, s));
-  NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
+  NK(h, coll_allreduce(h, h->c, mc, ncclFloat64, ncclSum, s));
   h->stats.launches += 1;
   // inner loop: sweep launches enqueued in chunks; each launch first applies the stop
   // test of the previous sweep on the device (global delta after its MAX all-reduce), so the host
@@ -873,9 +890,9 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
     for (int k = 0; k < chunk; ++k, ++enq) {
       CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
       CK(h, launch_proj(pa, h->grid, s));
-      NK(h, h->nccl->AllReduce(h->c, h->c, mc, ncclFloat64, ncclSum, h->comm, s));
+      NK(h, coll_allreduce(h, h->c, mc, ncclFloat64, ncclSum, s));
       if (eps2 > 0.0 || enq + 1 >= max_iter2)
-        NK(h, h->nccl->AllReduce(h->scal, h->scal, 1, ncclFloat64, ncclMax, h->comm, s));
+        NK(h, coll_allreduce(h, h->scal, 1, ncclFloat64, ncclMax, s));
       h->stats.launches += 1;
     }
     if (eps2 > 0.0 && enq < max_iter2) {
@@ -890,10 +907,10 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
   pa.tile_ctr = nullptr;       // the finalize phases tile by rows of X (static)
   pa.mode = kProjFinMu;
   CK(h, launch_proj(pa, h->grid, s));
-  NK(h, h->nccl->AllReduce(h->scal + 1, h->scal + 1, 1, ncclFloat64, ncclMax, h->comm, s));
+  NK(h, coll_allreduce(h, h->scal + 1, 1, ncclFloat64, ncclMax, s));
   pa.mode = kProjFinApply;
   CK(h, launch_proj(pa, h->grid, s));
-  NK(h, h->nccl->AllReduce(h->scal + 2, h->scal + 2, 1, ncclFloat64, ncclMax, h->comm, s));
+  NK(h, coll_allreduce(h, h->scal + 2, 1, ncclFloat64, ncclMax, s));
   h->stats.launches += 2;
   h->stats.proj_launches += 1;
   if (h->profile) CK(h, cudaEventRecord(h->ev[2], s));
@@ -935,6 +952,7 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
       R.delta_trace = rep->delta_trace; R.mu_trace = rep->mu_trace;
     }
     CK(h, cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    h->coll_log.clear();
     for (int32_t k = 0; k < max_iter1; ++k) {
       DevIter it{};
       int rc = dist_outer(h, alpha, lambda, eps1, eps2, max_iter2, it);
@@ -1104,6 +1122,15 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
   return FASTPFP_OK;
 }
 
+int fastpfp_dist_collectives(fastpfp_handle* h, int64_t* out, int64_t capacity, int64_t* count) {
+  GUARD(h);
+  if (!count || (capacity > 0 && !out)) return FASTPFP_EINVAL;
+  *count = (int64_t)h->coll_log.size();
+  for (int64_t k = 0; k < std::min<int64_t>(capacity, *count); ++k)
+    for (int q = 0; q < 4; ++q) out[4 * k + q] = h->coll_log[k][q];
+  return FASTPFP_OK;
+}
+
 int fastpfp_get_stats(fastpfp_handle* h, fastpfp_stats* out) {
   GUARD(h);
   if (!out) return FASTPFP_EINVAL;
@@ -1153,11 +1180,12 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   if (!h->dot_part) CK(h, alloc_arr(h->dot_part, 2 * (size_t)kDotBlocks));
   cudaStream_t s = h->stream;
   if (h->dist) {
+    h->coll_log.clear();
     int rc = dist_gemms(h, lambda, h->G.p, h->G.ld, false);
     if (rc) return rc;
     CK(h, launch_dot2(h->X.p, h->G.p, h->d > 0 ? h->K.p : nullptr, h->X.ld, (int)h->n, (int)h->np,
                       h->dot_part, h->scal + 4, s));
-    NK(h, h->nccl->AllReduce(h->scal + 4, h->scal + 4, 2, ncclFloat64, ncclSum, h->comm, s));
+    NK(h, coll_allreduce(h, h->scal + 4, 2, ncclFloat64, ncclSum, s));
     double* v = h->hpin + 4;
     CK(h, cudaMemcpyAsync(v, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     rc = stream_sync(h);
@@ -1182,9 +1210,10 @@ int fastpfp_discretize(fastpfp_handle* h, int32_t* assign) {
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   std::string msg;
   if (h->dist) {   // gather the full X (every rank gets the same greedy result)
+    h->coll_log.clear();
     if (!h->Xall.p) CK(h, alloc_buf(h->Xall, (int)h->n_glob, (int)h->np));
     const size_t cnt = (size_t)h->n * h->X.ld;
-    NK(h, h->nccl->AllGather(h->X.p, h->Xall.p, cnt, ncclFloat32, h->comm, h->stream));
+    NK(h, coll_allgather(h, h->X.p, h->Xall.p, cnt, ncclFloat32, h->stream));
     int rc = stream_sync(h);
     if (rc) return rc;
     rc = fpfp_discretize_device(&h->greedy, h->Xall.p, h->Xall.ld, (int)h->n_glob, (int)h->np, assign,

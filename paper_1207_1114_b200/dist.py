@@ -82,3 +82,44 @@ def local_inputs(problem, shard: RowShard):
     A = np.ascontiguousarray(problem.A[shard.sl])
     B = None if problem.B is None else np.ascontiguousarray(problem.B[shard.sl])
     return A, problem.Ap, B, problem.Bp
+
+
+# ------------------------------------------------------------------------------------------------
+# The collective schedule of one sharded outer iteration
+# ------------------------------------------------------------------------------------------------
+# Entries are (kind, dtype, op, count) with NCCL's enum values, the encoding
+# fastpfp_dist_collectives reports: kind 0 = all-reduce, 1 = all-gather; op -1 for all-gathers.
+ALL_REDUCE, ALL_GATHER = 0, 1
+NCCL_INT8, NCCL_UINT32, NCCL_FLOAT32, NCCL_FLOAT64 = 0, 3, 7, 8
+NCCL_SUM, NCCL_MAX = 0, 2
+
+
+def _round_up(x: int, q: int) -> int:
+    return (x + q - 1) // q * q
+
+
+def collective_schedule(n: int, n_prime: int, world: int, int8: bool, eps2: float, sweeps: int):
+    """The collectives one outer iteration of the row-sharded path issues, in order, when its inner
+    loop makes `sweeps` sweep launches (the fixed count when eps2 == 0):
+      GEMM1 -> [int8: MAX of U's per-row |max| (n' uint32); all-gather of U's 3 digit planes
+               (n' x round_up(n/P, 128) int8 each) | TF32: all-gather of U's big and small parts
+               (n' x round_up(n/P, 32) fp32 each)] -> GEMM2 ->
+      sums pass: SUM of [column sums | sigma] (m + 1 fp64) ->
+      per sweep: SUM of [column sums | sigma]; MAX of delta (1 fp64) when eps2 > 0 or on the last
+      sweep -> MAX of mu (1 fp64) -> MAX of rho (1 fp64)."""
+    rows = n // world
+    m = max(n, n_prime)
+    out = []
+    if int8:
+        out.append((ALL_REDUCE, NCCL_UINT32, NCCL_MAX, n_prime))
+        out += [(ALL_GATHER, NCCL_INT8, -1, n_prime * _round_up(rows, 128))] * 3
+    else:
+        out += [(ALL_GATHER, NCCL_FLOAT32, -1, n_prime * _round_up(rows, 32))] * 2
+    out.append((ALL_REDUCE, NCCL_FLOAT64, NCCL_SUM, m + 1))
+    for s in range(sweeps):
+        out.append((ALL_REDUCE, NCCL_FLOAT64, NCCL_SUM, m + 1))
+        if eps2 > 0.0 or s + 1 == sweeps:
+            out.append((ALL_REDUCE, NCCL_FLOAT64, NCCL_MAX, 1))
+    out.append((ALL_REDUCE, NCCL_FLOAT64, NCCL_MAX, 1))
+    out.append((ALL_REDUCE, NCCL_FLOAT64, NCCL_MAX, 1))
+    return out

@@ -152,3 +152,26 @@ def test_dist_nccl_timeout_aborts_and_poisons():
         s.iterate(p.alpha, p.lam, 0.0, 0.0, 1, 20)
     assert e.value.status == F.EPOISONED
     s.close()
+
+
+@pytest.mark.parametrize("prec", [pytest.param(0, id="tf32x3"), pytest.param(3, id="int8ozaki")])
+def test_dist_collective_sequence_matches_schedule(prec):
+    # the collectives the library issues per outer iteration (fastpfp_dist_collectives) are exactly
+    # dist.collective_schedule's — the sequence the gloo decomposition test executes on 2 ranks
+    import paper_1207_1114_b200 as F
+    from paper_1207_1114_b200 import dist as D
+    p = inputs.config5(n=1024)
+    s = _dist_solver(p)
+    s.set_option(F.OPT_PRECISION, prec)
+    s.set_graphs(p.A, p.Ap, p.B, p.Bp)
+    s.iterate(p.alpha, p.lam, 0.0, 0.0, 2, 7)
+    want = D.collective_schedule(p.n, p.n_prime, 1, prec == 3, 0.0, 7) * 2
+    assert s.collectives() == want
+    # eps2 > 0: sweeps are enqueued 8 at a time, each launch with its delta MAX; the log follows
+    # the schedule of the enqueued launches
+    s.iterate(p.alpha, p.lam, 0.0, 1e-9, 1, 20)
+    log = s.collectives()
+    n_sweeps = sum(1 for e in log if e == (D.ALL_REDUCE, D.NCCL_FLOAT64, D.NCCL_SUM, p.n + 1)) - 1
+    assert n_sweeps in (8, 16, 20)
+    assert log == D.collective_schedule(p.n, p.n_prime, 1, prec == 3, 1e-9, n_sweeps)
+    s.close()
