@@ -74,8 +74,11 @@ struct I8Params {
   const int* done;
 };
 
+#ifndef FPFP_I8_GROUP
+#define FPFP_I8_GROUP 8   // M tiles per raster group (experiment switch)
+#endif
 __device__ __forceinline__ void tile_coords_i8(int t, int num_m, int num_n, int& mt, int& nt) {
-  constexpr int kGroup = 8;
+  constexpr int kGroup = FPFP_I8_GROUP;
   const int per_group = kGroup * num_n;
   const int g = t / per_group;
   const int first_m = g * kGroup;
