@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fastpfp.h"
 #include "common.cuh"
 #include "nccl_dyn.h"
@@ -116,6 +118,13 @@ struct fastpfp_handle {
 };
 
 namespace {
+
+// NVTX range for the duration of a C-ABI call (header-only NVTX 3: a no-op unless a profiler such as
+// nsys is attached), so traces show set_graphs / iterate / discretize around their kernels
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int set_err(fastpfp_handle* h, int code, const char* fmt, ...) {
   if (h) {
@@ -706,6 +715,7 @@ int fastpfp_set_ga_schedule(fastpfp_handle* h, double beta0, double rate, double
 int fastpfp_set_graphs(fastpfp_handle* h, const float* A, const float* A_prime, const float* B,
                        const float* B_prime, int is_device) {
   GUARD(h);
+  NvtxRange nvtx_("fastpfp_set_graphs");
   if (!A || !A_prime) return set_err(h, FASTPFP_EINVAL, "A and A' are required");
   if (h->d > 0 && (!B || !B_prime)) return set_err(h, FASTPFP_EINVAL, "B and B' required (d > 0)");
   cudaStream_t s = h->stream;
@@ -942,6 +952,7 @@ static int dist_outer(fastpfp_handle* h, double alpha, double lambda, double eps
 int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1, double eps2,
                     int32_t max_iter1, int32_t max_iter2, float* X_out, fastpfp_report* rep) {
   GUARD(h);
+  NvtxRange nvtx_("fastpfp_iterate");
   if (h->dist && h->graphs_set && (alpha >= 0.0 && alpha <= 1.0) && lambda >= 0.0 &&
       std::isfinite(lambda) && eps1 >= 0.0 && eps2 >= 0.0 && max_iter1 >= 1 && max_iter2 >= 1) {
     if (h->precision == 2) return set_err(h, FASTPFP_EUNSUPPORTED, "row sharding needs the tensor-core GEMM");
@@ -1174,6 +1185,7 @@ int fastpfp_set_y(fastpfp_handle* h, const float* Y, int is_device) {
 
 int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
   GUARD(h);
+  NvtxRange nvtx_("fastpfp_objective");
   if (!f) return FASTPFP_EINVAL;
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   if (!h->G.p) CK(h, alloc_buf(h->G, (int)h->n, (int)h->np));
@@ -1206,6 +1218,7 @@ int fastpfp_objective(fastpfp_handle* h, double lambda, double* f) {
 
 int fastpfp_discretize(fastpfp_handle* h, int32_t* assign) {
   GUARD(h);
+  NvtxRange nvtx_("fastpfp_discretize");
   if (!assign) return FASTPFP_EINVAL;
   if (!h->graphs_set) return set_err(h, FASTPFP_ESTATE, "fastpfp_set_graphs must come first");
   std::string msg;
