@@ -281,7 +281,7 @@ def run_ours(args):
 
     p = make_problem(args.workload)
     inner = p.max_iter2 if args.workload == "c5" else 20
-    sharded = world > 1 and args.workload == "c5"
+    sharded = (world > 1 or args.force_shard) and args.workload == "c5"
     if sharded:
         # row-sharded pair (BASELINE configs[4]): this rank owns n/P rows; NCCL over NVLink
         shard = D.row_partition(p.n, p.n_prime, world, rank)
@@ -901,6 +901,9 @@ def main(argv=None):
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launcher-selftest", action="store_true", help=argparse.SUPPRESS)
+    # run c5 through the row-sharded handle even on one rank (exercises the multi-GPU code path of
+    # this script — shard inputs, e2e, full match — on a single GPU)
+    ap.add_argument("--force-shard", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch(argv, args.gpus))
