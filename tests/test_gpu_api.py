@@ -113,3 +113,12 @@ def test_default_precision_is_int8_ozaki():
         outs.append(X)
         s.close()
     assert np.array_equal(outs[0], outs[1])
+    # the handle reports the precision it chose; past the int8 digit sums' K limit it is 3xTF32
+    s = F.Solver(p.n, p.n_prime, p.d)
+    assert s.get_option(F.OPT_PRECISION) == F.PREC_INT8_OZAKI
+    s.set_option(F.OPT_PRECISION, F.PREC_TF32X3)
+    assert s.get_option(F.OPT_PRECISION) == F.PREC_TF32X3
+    s.close()
+    big = F.Solver(40000, 8, 0)
+    assert big.get_option(F.OPT_PRECISION) == F.PREC_TF32X3
+    big.close()
