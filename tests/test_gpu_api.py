@@ -119,6 +119,6 @@ def test_default_precision_is_int8_ozaki():
     s.set_option(F.OPT_PRECISION, F.PREC_TF32X3)
     assert s.get_option(F.OPT_PRECISION) == F.PREC_TF32X3
     s.close()
-    big = F.Solver(40000, 8, 0)
+    big = F.Solver(32769, 8, 0)
     assert big.get_option(F.OPT_PRECISION) == F.PREC_TF32X3
     big.close()
