@@ -150,14 +150,16 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
       }
       const double rs = (s0 + s1) + (s2 + s3);
-      p.rowp[((int64_t)buf * p.PC + pc) * p.m + r0 + t] = rs;
+      if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
+      else p.rowp[((int64_t)buf * p.PC + pc) * p.m + r0 + t] = rs;
       rsum += rs;
     }
     for (int j = threadIdx.x; j < nc; j += kThreads) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
-      p.colp[((int64_t)buf * p.PR + pr) * p.m + c0 + j] = s;
+      if (nb == 1) sh.c[j] = s;
+      else p.colp[((int64_t)buf * p.PR + pr) * p.m + c0 + j] = s;
     }
     rsum = warp_sum(rsum);
     if (lane == 0) sh.red[warp] = rsum;
@@ -166,8 +168,13 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       double t = 0.0;
       float d = 0.0f;
       for (int w = 0; w < kWarps; ++w) { t += sh.red[w]; d = fmaxf(d, sh.dred[w]); }
-      p.tot[buf * nb + b] = t;
-      p.dlt[buf * nb + b] = d;
+      if (nb == 1) {
+        sh.bc[0] = t;
+        sh.bc[1] = (double)d;
+      } else {
+        p.tot[buf * nb + b] = t;
+        p.dlt[buf * nb + b] = d;
+      }
     }
 #ifdef FPFP_OC_PROF
     pc_cols += clock64() - c1_;
@@ -251,12 +258,22 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
     __syncthreads();
   };
 
+  // a single tile (m <= kOnchipSingleTile) needs no exchange: its sums are already in shared memory
+  auto exchange = [&](int bufx, double& sigma_, float& delta_) {
+    if (nb == 1) {
+      __syncthreads();
+      sigma_ = sh.bc[0];
+      delta_ = (float)sh.bc[1];
+      return;
+    }
+    exchange_barrier();
+    absorb(bufx, sigma_, delta_);
+  };
   int buf = 0;
   double sigma;
   float delta;
   pass(false, buf, 0.0);
-  exchange_barrier();
-  absorb(buf, sigma, delta);
+  exchange(buf, sigma, delta);
 
   int sweeps = 0;
 #ifdef FPFP_OC_PROF
@@ -269,12 +286,18 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #ifdef FPFP_OC_PROF
     const long long b0_ = clock64();
 #endif
-    exchange_barrier();
+    if (nb > 1) exchange_barrier();
 #ifdef FPFP_OC_PROF
     const long long b1_ = clock64();
     pc_bar += b1_ - b0_;
 #endif
-    absorb(buf, sigma, delta);
+    if (nb > 1) {
+      absorb(buf, sigma, delta);
+    } else {
+      __syncthreads();
+      sigma = sh.bc[0];
+      delta = (float)sh.bc[1];
+    }
 #ifdef FPFP_OC_PROF
     pc_abs += clock64() - b1_;
 #endif
@@ -391,11 +414,14 @@ static KernFn onchip_kernel_for(int TCo) {
   }
 }
 
+#ifndef FPFP_OC_SINGLE_TILE
+#define FPFP_OC_SINGLE_TILE 128   // m up to which the whole Y is one CTA's tile (no grid exchange)
+#endif
 bool onchip_fits(int m, int num_sms, int& PR, int& PC, int& TRo, int& TCo) {
   int side = 1;
   while ((side + 1) * (side + 1) <= num_sms) ++side;          // 12 x 12 on 148 SMs
   const int want = (int)ceil_div(m, 32);                      // at least 32 x 32 per tile
-  PR = PC = std::max(1, std::min(side, want));
+  PR = PC = m <= FPFP_OC_SINGLE_TILE ? 1 : std::max(1, std::min(side, want));
   TRo = (int)ceil_div(m, PR);
   TCo = (int)round_up(ceil_div(m, PC), 4);
   if (TCo > kOnchipMaxTC || TRo > kOnchipMaxTC || PR * PC > 160 || PR > 12 || PC > 12) return false;
