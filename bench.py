@@ -541,8 +541,10 @@ def secondary_pair(name, method=0):
             "solve_ms": round(solve_ms, 3), "full_match_wall_ms": round(wall * 1e3, 3),
             "planted_recovery": acc, "ms_per_sweep": round(solve_ms / max(rep.total_sweeps, 1), 5),
             "bound": "latency (L2/on-chip resident working set; one grid exchange per sweep)",
-            "proj_kernel": ("on-chip tiles (%d CTAs, 1 grid barrier per sweep)" % st["onchip_tiles"]
-                            if st["onchip_launches"] else "streaming (2 grid barriers per sweep)"),
+            "proj_kernel": (("on-chip tiles (%d CTAs, one tagged-record exchange per sweep, no grid barrier)"
+                             % st["onchip_tiles"]) if st["onchip_tiles"] > 1 else
+                            "on-chip, one CTA holds Y (no exchange)")
+                           if st["onchip_launches"] else "streaming (2 grid barriers per sweep)",
             "paper_context": "a few seconds for 1000-node graphs on a 3 GHz Core2 PC in MATLAB (PAPER.md:33-34)"}
 
 

@@ -78,7 +78,7 @@ struct fastpfp_handle {
   int PR = 1, PC = 1, TRo = 1, TCo = 4;
   double *oc_rowp = nullptr, *oc_colp = nullptr, *oc_tot = nullptr;
   float* oc_dlt = nullptr;
-  unsigned* oc_bar = nullptr;
+  unsigned oc_epoch = 0;           // launch counter: the exchange records' tag epoch
   // Ozaki int8 operands (FASTPFP_OPT_PRECISION = 3, gemm_i8.cu), allocated on first use
   I8Buf Ai8, Api8, Xi8, Ui8, Ui8all;   // Ui8all: gathered U digit planes [world][n'][n/P] (sharded)
   unsigned* Urowmax = nullptr;
@@ -497,7 +497,7 @@ void fastpfp_destroy(fastpfp_handle* h) {
                   (void*)h->iters, (void*)h->done, (void*)h->flags, (void*)h->scal, (void*)h->dot_part,
                   (void*)h->inner, (void*)h->tile_ctr,
                   (void*)h->oc_rowp, (void*)h->oc_colp, (void*)h->oc_tot, (void*)h->oc_dlt,
-                  (void*)h->oc_bar, (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
+                  (void*)h->ga_E, (void*)h->ga_u, (void*)h->ga_v,
                   (void*)h->ga_dlt, (void*)h->ga_rho})
     if (p) cudaFree(p);
   if (h->h_iters) cudaFreeHost(h->h_iters);
@@ -560,9 +560,9 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   if (!dist && onchip_fits((int)h->m, h->num_sms, h->PR, h->PC, h->TRo, h->TCo)) {
     const int nb = h->PR * h->PC;
     h->oc_ok = true;
-    A(alloc_arr(h->oc_rowp, 2 * (size_t)h->PC * M)); A(alloc_arr(h->oc_colp, 2 * (size_t)h->PR * M));
-    A(alloc_arr(h->oc_tot, 2 * (size_t)nb)); A(alloc_arr(h->oc_dlt, 2 * (size_t)nb));
-    A(alloc_arr(h->oc_bar, 1));
+    // tagged 16-byte exchange records (proj_onchip.cu): 2 doubles / 4 floats of storage each
+    A(alloc_arr(h->oc_rowp, 4 * (size_t)h->PC * M)); A(alloc_arr(h->oc_colp, 4 * (size_t)h->PR * M));
+    A(alloc_arr(h->oc_tot, 4 * (size_t)nb)); A(alloc_arr(h->oc_dlt, 8 * (size_t)nb));
     if (nb > h->grid) {   // mu/rho partials are indexed by tile
       cudaFree(h->mu_part); cudaFree(h->rho_part);
       h->mu_part = nullptr; h->rho_part = nullptr;
@@ -1058,8 +1058,9 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
         oa.PR = h->PR; oa.PC = h->PC; oa.TRo = h->TRo; oa.TCo = h->TCo;
         oa.rowp = h->oc_rowp; oa.colp = h->oc_colp; oa.tot = h->oc_tot; oa.dlt = h->oc_dlt;
         oa.mu_part = h->mu_part; oa.rho_part = h->rho_part; oa.iter_out = h->iters + k;
-        oa.done = h->done; oa.bar = h->oc_bar;
-        CK(h, cudaMemsetAsync(h->oc_bar, 0, sizeof(unsigned), s));
+        oa.done = h->done;
+        if (((++h->oc_epoch) & 0xffffu) == 0) ++h->oc_epoch;   // tags of the exchange records
+        oa.epoch = h->oc_epoch;
         CK(h, launch_proj_onchip(oa, s));
         h->stats.launches += 1;
         h->stats.proj_launches += 1;

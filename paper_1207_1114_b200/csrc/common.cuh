@@ -82,13 +82,15 @@ struct OnchipArgs {
   double alpha, eps1, eps2;
   int max_iter2, rescale, do_finalize;
   int PR, PC, TRo, TCo;          // tile grid and tile extent
-  double* rowp;                  // [2][PC][m] row partials
+  // exchange buffers, each value a 16-byte tagged record {lo32, tag, hi32, tag} (tag = the
+  // launch epoch and sweep: the reader polls until both tags match, no barrier)
+  double* rowp;                  // [2][PC][m] row partials (2 doubles of storage per record)
   double* colp;                  // [2][PR][m] column partials
   double* tot;                   // [2][PR*PC] tile totals
-  float* dlt;                    // [2][PR*PC] tile deltas
+  float* dlt;                    // [2][PR*PC] tile deltas (4 floats of storage per record)
+  unsigned epoch;                // launch epoch (host counter, never 0 mod 2^16)
   double* mu_part;               // [PR*PC]
   float* rho_part;               // [PR*PC]
-  unsigned* bar;                 // exchange barrier counter (zeroed before each launch)
   DevIter* iter_out;
   int* done;
 };

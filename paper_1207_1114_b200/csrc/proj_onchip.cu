@@ -6,10 +6,13 @@
 //
 // Each sweep: update the own tile with the row sums r_i (own rows), column sums c_j (own columns)
 // and sigma of the previous Y; emit fp64 partial row/column sums of the new tile, its total and its
-// delta to a double-buffered global exchange; ONE grid barrier; every CTA then re-reduces just the
-// partials of its own rows / columns (PC and PR values each) and the PR*PC totals in a fixed order,
-// so every CTA holds bit-identical r, c, sigma and delta (deterministic, no float atomics). The
-// streaming kernel (proj.cu) needs two barriers per sweep; at n ~ 1000 the barrier is the cost.
+// delta to a double-buffered global exchange; every CTA then re-reduces just the partials of its
+// own rows / columns (PC and PR values each) and the PR*PC totals in a fixed order, so every CTA
+// holds bit-identical r, c, sigma and delta (deterministic, no float atomics). At n ~ 1000 the
+// exchange is the cost, so it has no grid barrier: every exchanged value travels as a tagged
+// 16-byte record {lo32 | tag << 32, hi32 | tag << 32} (two single-copy-atomic 64-bit words, tag =
+// launch epoch and sweep), and a reader polls the records it needs until both tags match, so the
+// synchronisation and the data share one L2 round trip.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -40,6 +43,57 @@ struct OcShared {
   float dred[kWarps];
   double bc[4];
 };
+
+// tagged exchange records (see the header): written and polled with .relaxed.gpu 64-bit words
+__device__ __forceinline__ void st_tagged(void* dst, double v, unsigned tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long t = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(dst), "l"((u & 0xffffffffull) | t),
+               "l"((u >> 32) | t) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_tagged(const void* src) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(src) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool has_tag(const ulonglong2& v, unsigned tag) {
+  return (unsigned)(v.x >> 32) == tag && (unsigned)(v.y >> 32) == tag;
+}
+__device__ __forceinline__ double tagged_value(const ulonglong2& v) {
+  return __longlong_as_double((long long)((v.x & 0xffffffffull) | (v.y << 32)));
+}
+
+#ifndef FPFP_OC_POLL_NS
+#define FPFP_OC_POLL_NS 0
+#endif
+__device__ __forceinline__ void poll_backoff() {   // between re-polls of stale records
+  if (FPFP_OC_POLL_NS > 0) __nanosleep(FPFP_OC_POLL_NS);
+}
+
+// the first `count` records src[q * stride] into v (the rest: a tagged zero, never re-polled)
+template <int N>
+__device__ __forceinline__ void issue_tagged(ulonglong2 (&v)[N], const ulonglong2* src, int64_t stride, int count,
+                                             unsigned tag) {
+  const unsigned long long z = (unsigned long long)tag << 32;
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = q < count ? ld_tagged(src + q * stride) : make_ulonglong2(z, z);
+}
+// re-load the records whose tags are stale; true when none was
+template <int N>
+__device__ __forceinline__ bool repoll_tagged(ulonglong2 (&v)[N], const ulonglong2* src, int64_t stride, unsigned tag) {
+  bool ready = true;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (!has_tag(v[q], tag)) { ready = false; v[q] = ld_tagged(src + q * stride); }
+  return ready;
+}
+template <int N>
+__device__ __forceinline__ double sum_tagged(const ulonglong2 (&v)[N]) {   // in q order
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < N; ++q) s += tagged_value(v[q]);
+  return s;
+}
 
 template <int NQ>   // column chunks of 32 per lane: TCo <= 32 * NQ
 __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) {
@@ -80,7 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #ifdef FPFP_OC_PROF
   long long pc_rows = 0, pc_cols = 0;
 #endif
-  auto pass = [&](bool update, int buf, double tconst) {
+  ulonglong2* const rowq = reinterpret_cast<ulonglong2*>(p.rowp);   // [2][PC][m] records
+  ulonglong2* const colq = reinterpret_cast<ulonglong2*>(p.colp);   // [2][PR][m]
+  ulonglong2* const totq = reinterpret_cast<ulonglong2*>(p.tot);    // [2][nb]
+  ulonglong2* const dltq = reinterpret_cast<ulonglong2*>(p.dlt);    // [2][nb]
+  const unsigned tag0 = p.epoch << 16;                               // tag = tag0 ^ exchange index
+  auto pass = [&](bool update, int buf, unsigned tag, double tconst) {
 #ifdef FPFP_OC_PROF
     const long long c0_ = clock64();
 #endif
@@ -151,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       }
       const double rs = (s0 + s1) + (s2 + s3);
       if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
-      else p.rowp[((int64_t)buf * p.PC + pc) * p.m + r0 + t] = rs;
+      else st_tagged(rowq + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, rs, tag);
       rsum += rs;
     }
     for (int j = threadIdx.x; j < nc; j += kThreads) {
@@ -159,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
       if (nb == 1) sh.c[j] = s;
-      else p.colp[((int64_t)buf * p.PR + pr) * p.m + c0 + j] = s;
+      else st_tagged(colq + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, s, tag);
     }
     rsum = warp_sum(rsum);
     if (lane == 0) sh.red[warp] = rsum;
@@ -172,142 +231,113 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         sh.bc[0] = t;
         sh.bc[1] = (double)d;
       } else {
-        p.tot[buf * nb + b] = t;
-        p.dlt[buf * nb + b] = d;
+        st_tagged(totq + buf * nb + b, t, tag);
+        st_tagged(dltq + buf * nb + b, (double)d, tag);
       }
     }
 #ifdef FPFP_OC_PROF
     pc_cols += clock64() - c1_;
 #endif
+    __syncwarp();   // reconverge after the thread-0 / per-row branches (see the note in absorb)
   };
 
   // r (own rows), c (own columns), sigma, delta from exchange buffer `buf`, in a fixed order.
-  // Every load is independent and issued before any is consumed (one L2 round trip): thread t
-  // sums the PC partials of row t and the PR partials of column t in registers; warp 7 sums the
-  // tile totals and deltas. Loads bypass L1 (__ldcg): the buffers are rewritten every other sweep.
+  // Every record is loaded before any is consumed (one L2 round trip when the writers are done);
+  // a record whose tags are stale is re-polled. Row t's PC partials, column t's PR partials and
+  // (one warp) the PR*PC tile totals and deltas; with 512 threads rows and columns are polled by
+  // different halves of the block (register budget), with 256 by the same threads.
   constexpr int kMaxTilesPerLane = 5;   // PR * PC <= 160
   constexpr int kMaxP = 12;             // PR, PC <= 12
-  auto absorb = [&](int buf, double& sigma, float& delta) {
+  constexpr bool kSplit = kThreads >= 512;
+  auto absorb = [&](int buf, unsigned tag, double& sigma, float& delta) {
     const int t = threadIdx.x;
-    double rv[kMaxP], cv[kMaxP];
-    const double* rsrc = p.rowp + (int64_t)buf * p.PC * p.m + r0 + t;
-    const double* csrc = p.colp + (int64_t)buf * p.PR * p.m + c0 + t;
-#pragma unroll
-    for (int q = 0; q < kMaxP; ++q) {
-      rv[q] = (t < nr && q < p.PC) ? __ldcg(rsrc + (int64_t)q * p.m) : 0.0;
-      cv[q] = (t < nc && q < p.PR) ? __ldcg(csrc + (int64_t)q * p.m) : 0.0;
-    }
-    double tv[kMaxTilesPerLane];
-    float dv[kMaxTilesPerLane];
-    if (warp == kWarps - 1) {
-#pragma unroll
-      for (int u = 0; u < kMaxTilesPerLane; ++u) {
-        const int k = lane + 32 * u;
-        tv[u] = k < nb ? __ldcg(p.tot + buf * nb + k) : 0.0;
-        dv[u] = k < nb ? __ldcg(p.dlt + buf * nb + k) : 0.0f;
+    const ulonglong2* rsrc = rowq + (int64_t)buf * p.PC * p.m + r0 + t;
+    const ulonglong2* csrc = colq + (int64_t)buf * p.PR * p.m + c0 + (kSplit ? t - kThreads / 2 : t);
+    const ulonglong2* tsrc = totq + buf * nb + lane;
+    const ulonglong2* dsrc = dltq + buf * nb + lane;
+    const int tw = kSplit ? kWarps / 2 - 1 : kWarps - 1;   // the warp that sums the tile totals
+    if (kSplit && t >= kThreads / 2) {
+      ulonglong2 cv[kMaxP];
+      const int nq = t - kThreads / 2 < nc ? p.PR : 0;
+      issue_tagged(cv, csrc, p.m, nq, tag);
+      while (!repoll_tagged(cv, csrc, p.m, tag)) poll_backoff();
+      __syncwarp();
+      if (nq) sh.c[t - kThreads / 2] = sum_tagged(cv);
+    } else {
+      ulonglong2 rv[kMaxP], cv[kSplit ? 1 : kMaxP], tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
+      const int nr_q = t < nr ? p.PC : 0, nc_q = (!kSplit && t < nc) ? p.PR : 0;
+      const int nt_q = warp == tw ? (nb - lane + 31) / 32 : 0;   // tiles lane, lane + 32, ...
+      issue_tagged(rv, rsrc, p.m, nr_q, tag);
+      issue_tagged(cv, csrc, p.m, nc_q, tag);
+      issue_tagged(tv, tsrc, 32, nt_q, tag);
+      issue_tagged(dv, dsrc, 32, nt_q, tag);
+      for (;;) {
+        bool ready = repoll_tagged(rv, rsrc, p.m, tag);
+        ready &= repoll_tagged(cv, csrc, p.m, tag);
+        ready &= repoll_tagged(tv, tsrc, 32, tag);
+        ready &= repoll_tagged(dv, dsrc, 32, tag);
+        if (ready) break;
+        poll_backoff();
       }
-    }
-    if (t < nr) {
-      double s = 0.0;
+      // the lanes of a warp leave the poll loop in different iterations: reconverge them here
+      // (with the __syncwarp at the end of pass, which follows thread-dependent branches) or the
+      // next element loop can run with its warps split (measured at c2: 5.2 us per sweep with
+      // neither, 4.6 with this one only, 3.5 with both)
+      __syncwarp();
+      if (nr_q) sh.r[t] = sum_tagged(rv);
+      if (nc_q) sh.c[t] = sum_tagged(cv);
+      if (warp == tw) {   // (converged: __syncwarp above)
+        double sv = sum_tagged(tv);
+        float d = 0.0f;
 #pragma unroll
-      for (int q = 0; q < kMaxP; ++q) s += rv[q];
-      sh.r[t] = s;
-    }
-    if (t < nc) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < kMaxP; ++q) s += cv[q];
-      sh.c[t] = s;
-    }
-    if (warp == kWarps - 1) {
-      double s = 0.0;
-      float d = 0.0f;
-#pragma unroll
-      for (int u = 0; u < kMaxTilesPerLane; ++u) { s += tv[u]; d = fmaxf(d, dv[u]); }
-      s = warp_sum(s);
-      d = warp_max(d);
-      if (lane == 0) { sh.bc[0] = s; sh.bc[1] = (double)d; }
+        for (int u = 0; u < kMaxTilesPerLane; ++u) d = fmaxf(d, (float)tagged_value(dv[u]));
+        sv = warp_sum(sv);
+        d = warp_max(d);
+        if (lane == 0) { sh.bc[0] = sv; sh.bc[1] = (double)d; }
+      }
     }
     __syncthreads();
     sigma = sh.bc[0];
     delta = (float)sh.bc[1];
   };
 
-  // Grid barrier for the exchange: a monotonic arrival counter (zeroed by the host before the
-  // launch), release on arrival, acquire on the poll (cheaper than cg::grid sync's fence + reset).
-  unsigned phase = 0;
-  auto exchange_barrier = [&]() {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      ++phase;
-      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.bar), "r"(1u) : "memory");
-      const unsigned target = (unsigned)nb * phase;
-      unsigned v;
-#ifdef FPFP_OC_RELAXED_POLL
-      // poll without acquire (an acquire load invalidates L1 on every try), then one acquire fence
-      do {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
-      } while (v < target);
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#else
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
-      } while (v < target);
-#endif
-    }
-    __syncthreads();
-  };
-
-  // a single tile (m <= kOnchipSingleTile) needs no exchange: its sums are already in shared memory
-  auto exchange = [&](int bufx, double& sigma_, float& delta_) {
+  // a single tile (m <= FPFP_OC_SINGLE_TILE) needs no exchange: its sums are already in shared memory
+  auto exchange = [&](int bufx, unsigned tag, double& sigma_, float& delta_) {
     if (nb == 1) {
       __syncthreads();
       sigma_ = sh.bc[0];
       delta_ = (float)sh.bc[1];
       return;
     }
-    exchange_barrier();
-    absorb(bufx, sigma_, delta_);
+    absorb(bufx, tag, sigma_, delta_);
   };
-  int buf = 0;
   double sigma;
   float delta;
-  pass(false, buf, 0.0);
-  exchange(buf, sigma, delta);
+  pass(false, 0, tag0, 0.0);               // exchange 0: the sums of the incoming Y
+  exchange(0, tag0, sigma, delta);
 
   int sweeps = 0;
 #ifdef FPFP_OC_PROF
-  long long pc_bar = 0, pc_abs = 0;
+  long long pc_abs = 0;
   pc_rows = pc_cols = 0;
 #endif
   for (;;) {
-    buf ^= 1;
-    pass(true, buf, (1.0 + sigma * inv_m) * inv_m);
+    const unsigned x = (unsigned)sweeps + 1;   // exchange index of this sweep (buffer x & 1)
+    pass(true, (int)(x & 1), tag0 ^ (x & 0xffffu), (1.0 + sigma * inv_m) * inv_m);
 #ifdef FPFP_OC_PROF
     const long long b0_ = clock64();
 #endif
-    if (nb > 1) exchange_barrier();
+    exchange((int)(x & 1), tag0 ^ (x & 0xffffu), sigma, delta);
 #ifdef FPFP_OC_PROF
-    const long long b1_ = clock64();
-    pc_bar += b1_ - b0_;
-#endif
-    if (nb > 1) {
-      absorb(buf, sigma, delta);
-    } else {
-      __syncthreads();
-      sigma = sh.bc[0];
-      delta = (float)sh.bc[1];
-    }
-#ifdef FPFP_OC_PROF
-    pc_abs += clock64() - b1_;
+    pc_abs += clock64() - b0_;
 #endif
     ++sweeps;
     if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;
   }
-#ifdef FPFP_OC_PROF
+#if defined(FPFP_OC_PROF) && !defined(FPFP_OC_PROF_NOPRINT)
   if ((b == 0 || b == nb - 1) && threadIdx.x == 0)
-    printf("oc-prof block %d: %d sweeps, clk/sweep: element loop %lld, partials %lld, barrier %lld, absorb %lld\n",
-           b, sweeps, pc_rows / sweeps, pc_cols / sweeps, pc_bar / sweeps, pc_abs / sweeps);
+    printf("oc-prof block %d: %d sweeps, clk/sweep: element loop %lld, partials %lld, exchange wait + absorb %lld\n",
+           b, sweeps, pc_rows / sweeps, pc_cols / sweeps, pc_abs / sweeps);
 #endif
 
   // write the tile back in fp32 (slack persists across outer iterations, reading A3)
