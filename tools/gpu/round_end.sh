@@ -14,3 +14,4 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:proj_kernel -c 1 -o gpurun_out/${T}_proj -f python tools/ncu_driver.py c5 1 > gpurun_out/${T}_ncu_proj.log 2>&1; echo "ncu proj rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:small_solve_tc -c 1 -o gpurun_out/${T}_c4 -f python tools/ncu_driver.py c4 20 > gpurun_out/${T}_ncu_c4.log 2>&1; echo "ncu c4 rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:rounds_kernel -c 1 -o gpurun_out/${T}_greedy -f python tools/ncu_driver.py discretize 16384 > gpurun_out/${T}_ncu_greedy.log 2>&1; echo "ncu greedy rc=$?"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:proj_onchip_kernel -c 1 -o gpurun_out/${T}_onchip -f python tools/ncu_driver.py c2 1 > gpurun_out/${T}_ncu_onchip.log 2>&1; echo "ncu onchip rc=$?"
