@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       const int j = lane + 32 * q;
       cj[q] = j < nc ? sh.c[j] * inv_m : 1e300;
     }
+    double tacc = 0.0;   // this lane's share of the tile total (published first, below)
     if (update) {
 #pragma unroll kRowUnroll
       for (int i = warp; i < nr; i += kWarps) {
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #pragma unroll
         for (int q = 0; q < NQ; ++q) row[32 * q] = z[q];
         rowacc[i * 33 + lane] = racc;
+        tacc += racc;
       }
     } else {
 #pragma unroll 2
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
           cacc[q] += y;
         }
         rowacc[i * 33 + lane] = racc;
+        tacc += racc;
       }
     }
     float dmax = 0.0f;
@@ -193,37 +196,12 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #pragma unroll
     for (int q = 0; q < NQ; ++q) sh.colsum[warp][lane + 32 * q] = cacc[q];
     dmax = warp_max(dmax);
-    if (lane == 0) sh.dred[warp] = dmax;
+    tacc = warp_sum(tacc);
+    if (lane == 0) { sh.dred[warp] = dmax; sh.red[warp] = tacc; }
     __syncthreads();
-#ifdef FPFP_OC_PROF
-    const long long c1_ = clock64();
-    pc_rows += c1_ - c0_;
-#endif
-    // row partials (own rows) and column partials (own columns), fixed order
-    double rsum = 0.0;
-    for (int t = threadIdx.x; t < nr; t += kThreads) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int l = 0; l < 32; l += 4) {
-        s0 += rowacc[t * 33 + l]; s1 += rowacc[t * 33 + l + 1];
-        s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
-      }
-      const double rs = (s0 + s1) + (s2 + s3);
-      if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
-      else st_tagged(rowq + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, rs, tag);
-      rsum += rs;
-    }
-    for (int j = threadIdx.x; j < nc; j += kThreads) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
-      if (nb == 1) sh.c[j] = s;
-      else st_tagged(colq + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, s, tag);
-    }
-    rsum = warp_sum(rsum);
-    if (lane == 0) sh.red[warp] = rsum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // the tile total and delta go out first: every CTA needs all of them, so they are the last
+    // records a reader waits for (the last thread rarely has a row or column of its own)
+    if (threadIdx.x == kThreads - 1) {
       double t = 0.0;
       float d = 0.0f;
       for (int w = 0; w < kWarps; ++w) { t += sh.red[w]; d = fmaxf(d, sh.dred[w]); }
@@ -236,9 +214,32 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       }
     }
 #ifdef FPFP_OC_PROF
+    const long long c1_ = clock64();
+    pc_rows += c1_ - c0_;
+#endif
+    // row partials (own rows) and column partials (own columns), fixed order
+    for (int t = threadIdx.x; t < nr; t += kThreads) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int l = 0; l < 32; l += 4) {
+        s0 += rowacc[t * 33 + l]; s1 += rowacc[t * 33 + l + 1];
+        s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
+      }
+      const double rs = (s0 + s1) + (s2 + s3);
+      if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
+      else st_tagged(rowq + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, rs, tag);
+    }
+    for (int j = threadIdx.x; j < nc; j += kThreads) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
+      if (nb == 1) sh.c[j] = s;
+      else st_tagged(colq + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, s, tag);
+    }
+#ifdef FPFP_OC_PROF
     pc_cols += clock64() - c1_;
 #endif
-    __syncwarp();   // reconverge after the thread-0 / per-row branches (see the note in absorb)
+    __syncwarp();   // reconverge after the per-thread branches (see the note in absorb)
   };
 
   // r (own rows), c (own columns), sigma, delta from exchange buffer `buf`, in a fixed order.
