@@ -108,9 +108,10 @@ typedef enum fastpfp_option {
   /* tensor-core GEMM tiling: 2 (default) = 256 x 256 tiles per CTA pair (tcgen05 cta_group::2),
    * 1 = 128 x 128 tiles per CTA (cta_group::1). Same arithmetic, same results up to ordering. */
   FASTPFP_OPT_GEMM_CTA_GROUP = 7,
-  /* projection kernel: 0 = auto (on-chip tiles with one grid barrier per sweep when Y fits in the
-   * aggregate shared memory, m <~ 2.2k; else streaming), 1 = streaming, 2 = on-chip (EUNSUPPORTED
-   * if Y does not fit). Same arithmetic; sums are reduced in a different fixed order. */
+  /* projection kernel: 0 = auto (on-chip tiles exchanging tagged partial-sum records once per sweep
+   * when Y fits in the aggregate shared memory, m <~ 2.2k; one CTA for m <= 128; else streaming),
+   * 1 = streaming, 2 = on-chip (EUNSUPPORTED if Y does not fit). Same arithmetic; sums are reduced
+   * in a different fixed order. */
   FASTPFP_OPT_PROJ_KERNEL = 8,
   /* 0 = FastPFP (Algorithm 1; default). 1 = Projected Gradient {pg}:
    * X <- P_d(X + alpha (A X A' + lambda K)), same projection, initialisation and stopping rules,
