@@ -13,7 +13,7 @@ import pytest
 from oracle import fastpfp as O
 from paper_1207_1114_b200 import inputs
 
-from .parity import assert_parity, run_pair
+from .parity import X_TOL, assert_parity, run_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -332,3 +332,17 @@ def test_distance_workload_parity(prec, dims):
     res = run_pair(p, prec)
     assert_parity(res)
     assert np.mean(res.assign_gpu == p.perm) >= 0.95
+
+
+@pytest.mark.parametrize("shape", [(129, 129, 2), (700, 333, 4), (1400, 1500, 4)])
+def test_onchip_tilings_lockstep(shape):
+    # the on-chip projection forced (OPT_PROJ_KERNEL = 2) over tilings the configs do not reach:
+    # m = 129 (the first multi-tile size: 5 x 5 tiles), m = 700 with slack columns, m = 1500 (12 x 12
+    # tiles of 125 x 128, 4 column chunks per lane, near the shared-memory limit). The tagged
+    # exchange of partial sums runs every sweep; lockstep parity with the oracle after each of the
+    # first 3 outer iterations (eps1 = 0, 40 sweeps cap: the tiles exchange 40 times per iteration).
+    n, npr, d = shape
+    p = inputs.planted_unequal(300 + n, n, npr, d=d, eps1=0.0, eps2=1e-7, max_iter1=3, max_iter2=40)
+    res = run_pair(p, 3, lockstep=3, proj_kernel=2)
+    assert max(res.lockstep_max) <= X_TOL, res.lockstep_max
+    assert all(abs(a - b) <= 1 for a, b in zip(res.gpu_sweeps, res.oracle_sweeps)), (res.gpu_sweeps, res.oracle_sweeps)
