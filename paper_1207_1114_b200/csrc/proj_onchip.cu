@@ -36,9 +36,13 @@ constexpr int kRowUnroll = FPFP_OC_UNROLL;   // rows of the element loop in flig
 constexpr int kWarps = kThreads / 32;
 
 struct OcShared {
-  double colsum[kWarps][kOnchipMaxTC];
+  union {                     // per-warp column partials: fp64 (sums pass, first sweep) or fp32
+    double d[kWarps][kOnchipMaxTC];
+    float f[kWarps][kOnchipMaxTC];
+  } colsum;
   double r[kOnchipMaxTC];     // own rows' sums
   double c[kOnchipMaxTC];     // own columns' sums
+  float uf[kOnchipMaxTC];     // fl32(c_j / m) for the fp32 sweeps (padding columns: 3e38)
   double red[kWarps];
   float dred[kWarps];
   double bc[4];
@@ -99,12 +103,16 @@ template <int NQ>   // column chunks of 32 per lane: TCo <= 32 * NQ
 __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) {
   if (*p.done) return;
   cg::grid_group grid = cg::this_grid();
-  // The tile is held in fp64 on chip (no per-sweep rounding: closer to the fp64 definition than
-  // the streaming kernel's fp32 storage); it is rounded to fp32 once, when written back.
+  // Storage and arithmetic. The tile is fp32, Y's storage precision. The sums pass after the GEMM
+  // and the launch's first sweep (which cancels the GEMM's large values down to the projection's
+  // scale) run in fp64: fp64 correction and sums, one rounding of z to fp32. The
+  // later sweeps operate on the projection's own output and run in fp32 (P1, P2, delta), with fp32
+  // partial sums over short chains (<= NQ values per lane then 4 lanes per chain for a row; the
+  // warp's rows for a column) combined in fp64 — the streaming kernel's precision class.
   // Rows of the shared tile are padded to kLdt = 32 NQ columns: padded entries are 0 and their
-  // column correction is +1e300, so P2 keeps them at 0 and the element loop needs no bounds test.
+  // column correction is huge (1e300 / 3e38), so P2 keeps them at 0 with no bounds test.
   constexpr int kLdt = 32 * NQ;
-  extern __shared__ __align__(16) double tile[];   // [TRo][kLdt]
+  extern __shared__ __align__(16) float tile[];   // [TRo][kLdt]
   __shared__ OcShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x;
@@ -118,19 +126,22 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   // load the tile
   for (int i = warp; i < nr; i += kWarps)
     for (int j = lane; j < kLdt; j += 32)
-      tile[i * kLdt + j] = j < nc ? (double)p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] : 0.0;
+      tile[i * kLdt + j] = j < nc ? p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] : 0.0f;
+  for (int j = nc + threadIdx.x; j < kLdt; j += kThreads) sh.uf[j] = 3.0e38f;
   __syncthreads();
 
-  // One fused pass over the tile: optionally apply the sweep (P1 then P2, fp64 correction, one
-  // rounding), and emit the fp64 row / column partial sums, the tile total and the tile delta of
-  // the resulting values to exchange buffer `buf`. Latency, not bandwidth, bounds this kernel at
-  // n ~ 1000, so the element loop carries no cross-lane reduction and no fp64
-  // max chain: warp w walks rows w, w+8, ...; lane l keeps its columns' partial sums in registers
-  // and writes its per-row partial to shared memory (rowacc[i][l]); the 32 lane partials of a row
-  // and the 8 warp partials of a column are then summed by one thread each, in a fixed order.
-  // P2 is a sign test (max(z, 0) for finite z), the delta is tracked in fp32: rounding is
-  // monotonic, so max_ij fl32(|dz|) = fl32(max_ij |dz|), the same value the fp64 max would give.
-  double* rowacc = tile + (size_t)p.TRo * kLdt;   // [TRo][33]
+  // One fused pass over the tile: the sums of the incoming Y (kSums) or one sweep (P1 then P2;
+  // kSweep64 in fp64, kSweep32 in fp32), and the row / column partial sums, the tile total and the
+  // tile delta of the resulting values to exchange buffer `buf`. Latency, not bandwidth, bounds this
+  // kernel at n ~ 1000, so the element loop carries no cross-lane reduction: warp w
+  // walks rows w, w+8, ...; lane l keeps its columns' partial sums in registers and writes its
+  // per-row partial to shared memory (rowacc[i][l]); the 32 lane partials of a row and the 8 warp
+  // partials of a column are then summed by one thread each, in a fixed order. P2 is a sign test /
+  // max with 0; the delta is tracked in fp32: rounding is monotonic, so max_ij fl32(|dz|) =
+  // fl32(max_ij |dz|).
+  enum { kSums = 0, kSweep64 = 1, kSweep32 = 2 };
+  double* rowacc = reinterpret_cast<double*>(tile + (size_t)p.TRo * kLdt);   // [TRo][33] fp64
+  float* rowacc_f = reinterpret_cast<float*>(rowacc);                        // [TRo][33] fp32 (same space)
 #ifdef FPFP_OC_PROF
   long long pc_rows = 0, pc_cols = 0;
 #endif
@@ -139,62 +150,101 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   ulonglong2* const totq = reinterpret_cast<ulonglong2*>(p.tot);    // [2][nb]
   ulonglong2* const dltq = reinterpret_cast<ulonglong2*>(p.dlt);    // [2][nb]
   const unsigned tag0 = p.epoch << 16;                               // tag = tag0 ^ exchange index
-  auto pass = [&](bool update, int buf, unsigned tag, double tconst) {
+  auto pass = [&](int mode, int buf, unsigned tag, double tconst) {
 #ifdef FPFP_OC_PROF
     const long long c0_ = clock64();
 #endif
-    double cacc[NQ], cj[NQ];
-    float dq[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      cacc[q] = 0.0;
-      dq[q] = 0.0f;
-      const int j = lane + 32 * q;
-      cj[q] = j < nc ? sh.c[j] * inv_m : 1e300;
-    }
+    float dmax = 0.0f;
     double tacc = 0.0;   // this lane's share of the tile total (published first, below)
-    if (update) {
+    if (mode == kSweep32) {
+      float uf[NQ], cacc[NQ], dq[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) { uf[q] = sh.uf[lane + 32 * q]; cacc[q] = 0.0f; dq[q] = 0.0f; }
+      // t_i of the warp's rows: lane k rounds row warp + kWarps k's (fp64 -> fp32 once per row)
+      const int myrow = warp + kWarps * lane;
+      const float tmine = myrow < nr ? (float)(tconst - sh.r[myrow] * inv_m) : 0.0f;
+      float taccf = 0.0f;
+      int k = 0;
 #pragma unroll kRowUnroll
-      for (int i = warp; i < nr; i += kWarps) {
-        const double ti = tconst - sh.r[i] * inv_m;
-        double* row = &tile[i * kLdt + lane];
-        double y[NQ], z[NQ];
+      for (int i = warp; i < nr; i += kWarps, ++k) {
+        const float ti = __shfl_sync(0xffffffffu, tmine, k);
+        float* row = &tile[i * kLdt + lane];
+        float y[NQ], z[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) y[q] = row[32 * q];
-        double racc = 0.0;
+        float racc = 0.0f;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          double v = (y[q] + ti) - cj[q];                          // P1 (fp64)
-          z[q] = __double2hiint(v) < 0 ? 0.0 : v;                  // P2
-          dq[q] = fmaxf(dq[q], (float)fabs(z[q] - y[q]));
+          z[q] = fmaxf((y[q] + ti) - uf[q], 0.0f);                 // P1 then P2 (fp32)
+          dq[q] = fmaxf(dq[q], fabsf(z[q] - y[q]));
           racc += z[q];
           cacc[q] += z[q];
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) row[32 * q] = z[q];
-        rowacc[i * 33 + lane] = racc;
-        tacc += racc;
+        rowacc_f[i * 33 + lane] = racc;
+        taccf += racc;
+      }
+      tacc = (double)taccf;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        dmax = fmaxf(dmax, dq[q]);
+        sh.colsum.f[warp][lane + 32 * q] = cacc[q];
       }
     } else {
-#pragma unroll 2
-      for (int i = warp; i < nr; i += kWarps) {
-        const double* row = &tile[i * kLdt + lane];
-        double racc = 0.0;
+      double cacc[NQ], cj[NQ];
+      float dq[NQ];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const double y = row[32 * q];
-          racc += y;
-          cacc[q] += y;
+      for (int q = 0; q < NQ; ++q) {
+        cacc[q] = 0.0;
+        dq[q] = 0.0f;
+        const int j = lane + 32 * q;
+        cj[q] = j < nc ? sh.c[j] * inv_m : 1e300;
+      }
+      if (mode == kSweep64) {
+#pragma unroll kRowUnroll
+        for (int i = warp; i < nr; i += kWarps) {
+          const double ti = tconst - sh.r[i] * inv_m;
+          float* row = &tile[i * kLdt + lane];
+          double y[NQ];
+          float z[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) y[q] = (double)row[32 * q];
+          double racc = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const double v = (y[q] + ti) - cj[q];                  // P1 (fp64)
+            z[q] = __double2hiint(v) < 0 ? 0.0f : (float)v;        // P2, one rounding to fp32
+            dq[q] = fmaxf(dq[q], (float)fabs((double)z[q] - y[q]));
+            racc += (double)z[q];                                  // sums of the stored values
+            cacc[q] += (double)z[q];
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) row[32 * q] = z[q];
+          rowacc[i * 33 + lane] = racc;
+          tacc += racc;
         }
-        rowacc[i * 33 + lane] = racc;
-        tacc += racc;
+      } else {
+#pragma unroll 2
+        for (int i = warp; i < nr; i += kWarps) {
+          const float* row = &tile[i * kLdt + lane];
+          double racc = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const double y = (double)row[32 * q];
+            racc += y;
+            cacc[q] += y;
+          }
+          rowacc[i * 33 + lane] = racc;
+          tacc += racc;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        dmax = fmaxf(dmax, dq[q]);
+        sh.colsum.d[warp][lane + 32 * q] = cacc[q];
       }
     }
-    float dmax = 0.0f;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) dmax = fmaxf(dmax, dq[q]);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) sh.colsum[warp][lane + 32 * q] = cacc[q];
     dmax = warp_max(dmax);
     tacc = warp_sum(tacc);
     if (lane == 0) { sh.dred[warp] = dmax; sh.red[warp] = tacc; }
@@ -219,21 +269,37 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #endif
     // row partials (own rows) and column partials (own columns), fixed order
     for (int t = threadIdx.x; t < nr; t += kThreads) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      double rs;
+      if (mode == kSweep32) {   // 8 fp32 chains of 4 lane partials, combined in fp64
+        double acc = 0.0;
 #pragma unroll
-      for (int l = 0; l < 32; l += 4) {
-        s0 += rowacc[t * 33 + l]; s1 += rowacc[t * 33 + l + 1];
-        s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
+        for (int l = 0; l < 32; l += 4) {
+          const float* v = &rowacc_f[t * 33 + l];
+          acc += (double)((v[0] + v[1]) + (v[2] + v[3]));
+        }
+        rs = acc;
+      } else {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 32; l += 4) {
+          s0 += rowacc[t * 33 + l]; s1 += rowacc[t * 33 + l + 1];
+          s2 += rowacc[t * 33 + l + 2]; s3 += rowacc[t * 33 + l + 3];
+        }
+        rs = (s0 + s1) + (s2 + s3);
       }
-      const double rs = (s0 + s1) + (s2 + s3);
       if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
       else st_tagged(rowq + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, rs, tag);
     }
     for (int j = threadIdx.x; j < nc; j += kThreads) {
       double s = 0.0;
+      if (mode == kSweep32) {
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) s += sh.colsum[w][j];
-      if (nb == 1) sh.c[j] = s;
+        for (int w = 0; w < kWarps; ++w) s += (double)sh.colsum.f[w][j];
+      } else {
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s += sh.colsum.d[w][j];
+      }
+      if (nb == 1) { sh.c[j] = s; sh.uf[j] = (float)(s * inv_m); }
       else st_tagged(colq + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, s, tag);
     }
 #ifdef FPFP_OC_PROF
@@ -263,7 +329,11 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       issue_tagged(cv, csrc, p.m, nq, tag);
       while (!repoll_tagged(cv, csrc, p.m, tag)) poll_backoff();
       __syncwarp();
-      if (nq) sh.c[t - kThreads / 2] = sum_tagged(cv);
+      if (nq) {
+        const double cs = sum_tagged(cv);
+        sh.c[t - kThreads / 2] = cs;
+        sh.uf[t - kThreads / 2] = (float)(cs * inv_m);
+      }
     } else {
       ulonglong2 rv[kMaxP], cv[kSplit ? 1 : kMaxP], tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
       const int nr_q = t < nr ? p.PC : 0, nc_q = (!kSplit && t < nc) ? p.PR : 0;
@@ -286,7 +356,11 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       // neither, 4.6 with this one only, 3.5 with both)
       __syncwarp();
       if (nr_q) sh.r[t] = sum_tagged(rv);
-      if (nc_q) sh.c[t] = sum_tagged(cv);
+      if (nc_q) {
+        const double cs = sum_tagged(cv);
+        sh.c[t] = cs;
+        sh.uf[t] = (float)(cs * inv_m);
+      }
       if (warp == tw) {   // (converged: __syncwarp above)
         double sv = sum_tagged(tv);
         float d = 0.0f;
@@ -314,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   };
   double sigma;
   float delta;
-  pass(false, 0, tag0, 0.0);               // exchange 0: the sums of the incoming Y
+  pass(kSums, 0, tag0, 0.0);               // exchange 0: the sums of the incoming Y
   exchange(0, tag0, sigma, delta);
 
   int sweeps = 0;
@@ -324,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #endif
   for (;;) {
     const unsigned x = (unsigned)sweeps + 1;   // exchange index of this sweep (buffer x & 1)
-    pass(true, (int)(x & 1), tag0 ^ (x & 0xffffu), (1.0 + sigma * inv_m) * inv_m);
+    pass(sweeps == 0 ? kSweep64 : kSweep32, (int)(x & 1), tag0 ^ (x & 0xffffu), (1.0 + sigma * inv_m) * inv_m);
 #ifdef FPFP_OC_PROF
     const long long b0_ = clock64();
 #endif
@@ -343,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 
   // write the tile back in fp32 (slack persists across outer iterations, reading A3)
   for (int i = warp; i < nr; i += kWarps)
-    for (int j = lane; j < nc; j += 32) p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] = (float)tile[i * kLdt + j];
+    for (int j = lane; j < nc; j += 32) p.Y[(int64_t)(r0 + i) * p.ldY + c0 + j] = tile[i * kLdt + j];
   if (!p.do_finalize) {
     if (b == 0 && threadIdx.x == 0) {
       p.iter_out->valid = 1; p.iter_out->sweeps = sweeps; p.iter_out->delta = (double)delta;
@@ -428,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 static size_t onchip_smem(int TRo, int TCo, int PR, int PC) {
   (void)PR; (void)PC;
   const size_t ldt = (size_t)round_up(TCo, 32);                      // kLdt of the kernel
-  return ((size_t)TRo * ldt + (size_t)TRo * 33) * sizeof(double);    // tile + lane row partials
+  return (size_t)TRo * ldt * sizeof(float) + (size_t)TRo * 33 * sizeof(double);   // tile + lane row partials
 }
 
 using KernFn = void (*)(OnchipArgs);

@@ -334,11 +334,12 @@ def test_distance_workload_parity(prec, dims):
     assert np.mean(res.assign_gpu == p.perm) >= 0.95
 
 
-@pytest.mark.parametrize("shape", [(129, 129, 2), (700, 333, 4), (1400, 1500, 4)])
+@pytest.mark.parametrize("shape", [(129, 129, 2), (700, 333, 4), (1400, 1500, 4), (2200, 2100, 4)])
 def test_onchip_tilings_lockstep(shape):
     # the on-chip projection forced (OPT_PROJ_KERNEL = 2) over tilings the configs do not reach:
     # m = 129 (the first multi-tile size: 5 x 5 tiles), m = 700 with slack columns, m = 1500 (12 x 12
-    # tiles of 125 x 128, 4 column chunks per lane, near the shared-memory limit). The tagged
+    # tiles of 125 x 128, 4 column chunks per lane), m = 2200 (184 x 184 tiles, 6 column chunks per
+    # lane, near the shared-memory limit of the fp32 tile). The tagged
     # exchange of partial sums runs every sweep; lockstep parity with the oracle after each of the
     # first 3 outer iterations (eps1 = 0, 40 sweeps cap: the tiles exchange 40 times per iteration).
     n, npr, d = shape
