@@ -14,7 +14,7 @@ F32, F64 = np.float32, np.float64
 
 
 class Twin32:
-    def __init__(self, A, Ap, B=None, Bp=None, X0=None, gemm="f32"):
+    def __init__(self, A, Ap, B=None, Bp=None, X0=None, gemm="f32", sweep_arith="f64"):
         self.A = np.asarray(A, F32)
         self.Ap = np.asarray(Ap, F32)
         self.n, self.n_prime = self.A.shape[0], self.Ap.shape[0]
@@ -27,6 +27,9 @@ class Twin32:
                   if X0 is None else np.array(X0, F32))
         self.Y = np.zeros((self.m, self.m), F32)
         self.gemm = gemm
+        # "f64": every sweep's P1 correction in float64 (the streaming kernel); "f32": only the first
+        # sweep after the product, the later ones in float32 (the on-chip kernel)
+        self.sweep_arith = sweep_arith
 
     def _product(self, lam):
         if self.gemm == "f64":   # exact product rounded once to fp32
@@ -42,8 +45,11 @@ class Twin32:
         while True:
             Y64 = self.Y.astype(F64)
             r = Y64.sum(1); c = Y64.sum(0); s = r.sum()
-            Z = Y64 + ((1.0 + s / m - r) / m)[:, None] - (c / m)[None, :]
-            Z = np.maximum(Z, 0.0).astype(F32)
+            t, u = (1.0 + s / m - r) / m, c / m
+            if self.sweep_arith == "f32" and sweeps > 0:
+                Z = np.maximum((self.Y + t.astype(F32)[:, None]) - u.astype(F32)[None, :], F32(0))
+            else:
+                Z = np.maximum(Y64 + t[:, None] - u[None, :], 0.0).astype(F32)
             delta = float(np.max(np.abs(Z - self.Y)))
             self.Y = Z
             sweeps += 1

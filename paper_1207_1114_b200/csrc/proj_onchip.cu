@@ -1,8 +1,9 @@
 // proj_onchip.cu — the projection loop (Algorithm 1 lines 4-7) plus blend/rescale
-// (lines 8-9) for m small enough that Y fits in the GPU's aggregate shared memory (m <~ 1.5k:
-// BASELINE configs[1] and [2], n ~ 1000). The arithmetic of proj.cu (fp64 sums and correction)
-// with a different schedule: Y is split into PR x PC tiles, one per CTA, read from HBM/L2 once, kept
-// in shared memory in fp64 across all sweeps (no per-sweep rounding to fp32) and written back once.
+// (lines 8-9) for m small enough that Y fits in the GPU's aggregate shared memory (m <~ 2.2k:
+// BASELINE configs[1] and [2], n ~ 1000). Y is split into PR x PC tiles, one per CTA, read from
+// HBM/L2 once, kept in shared memory (fp32, Y's storage precision) across all sweeps and written back
+// once. Sums are fp64 beyond short fp32 chains; the first sweep after the product (which cancels its
+// large values) is fp64 arithmetic, the later ones fp32 (see the note in the kernel).
 //
 // Each sweep: update the own tile with the row sums r_i (own rows), column sums c_j (own columns)
 // and sigma of the previous Y; emit fp64 partial row/column sums of the new tile, its total and its
