@@ -23,6 +23,7 @@ pw = inputs.planted_unequal(6, 260, 200, d=4)
 for prec in (0, 3):
     for pk in (0, 1):
         run(p1, prec, 0, pk); run(pu, prec, 0, pk); run(pw, prec, 0, pk)
+    run(inputs.planted_unequal(8, 700, 650, d=4), prec, 0, 2)   # on-chip, 12 x 12 tiles, tagged exchange
     run(pu, prec, 1)                      # PG
     run(inputs.ga_pair(3, 150, 170), prec, 2)   # FastGA
 run(p1, 2)                                # SIMT GEMM
