@@ -21,8 +21,7 @@
 //   copy of A digits overlapped with the U epilogue (U digits, row scales over the whole row) ->
 //   GEMM2 G = A U^T (TMEM) -> + lambda K -> fp32 staging -> Y registers (X block)
 //   [slot only] the projection sweeps (Y in registers: warp w owns rows 16w..16w+15, lane l the
-//   columns 4l..4l+3, packed as row pairs for the fp32x2 pipe; fp32 sums; after an outer
-//   iteration's first sweep the column part of P1 rides in a per-column offset) -> blend: the X
+//   columns 4l..4l+3 as two float2 pairs for the packed fp32x2 pipe; fp32 sums) -> blend: the X
 //   block of Y becomes X~ = (1-a) X + a Y, mu = max X~, X = X~/mu (global) and its digits (global).
 #include <algorithm>
 #include <cstdio>
@@ -41,15 +40,13 @@ constexpr int kST = 256;              // threads per slot
 constexpr int kS = 128;               // max n, n', m
 constexpr int kPW = kST / 32;         // warps per slot (8)
 constexpr int kPR = kS / kPW;         // rows of the Y register tile per warp (16)
-constexpr int kPQ = kPR / 2;          // row pairs per warp (8): the packed fp32x2 operands
 constexpr int kEC = kS / 2;           // epilogue columns per warp (2 warps per TMEM lane quarter)
 constexpr int kLdG = kS + 4;          // fp32 staging row stride
 constexpr int kPlane = kS * kS;       // one digit plane: 128 rows x 128 bytes (SWIZZLE_128B image)
 constexpr int kOperand = 3 * kPlane;  // 48 KB: the three planes of one operand
 
-struct __align__(16) SlotSm {
+struct SlotSm {
   float colp[2][kPW][kS];     // per-warp column partials of the sweeps (double buffered)
-  float rowp[kPW][32 * kPR];  // per-lane row partials, transposed through shared memory (swizzled)
   float csum[kS];             // combined column sums of the current sweep
   float rsum[2][kPW][kPR];    // row sums of each warp's rows (double buffered)
   float wsig[2][kPW];         // per-warp totals (sigma partials, double buffered)
@@ -206,52 +203,48 @@ __device__ __forceinline__ float product_to_smem(uint32_t tb, float rscale, cons
   return mx;
 }
 
-// Packed fp32x2 values as 64-bit registers (PTX .b64 operands of the f32x2 instructions): ptxas
-// then keeps each pair in an aligned register pair, where float2 temporaries were re-paired with
-// moves around every packed instruction.
-__device__ __forceinline__ uint64_t f2pk(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float f2lo(uint64_t v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return a;
-}
-__device__ __forceinline__ float f2hi(uint64_t v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return b;
-}
-__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-// (max(lo, c), max(hi, c)): there is no packed max, two FMNMX on the halves in place
-__device__ __forceinline__ uint64_t f2maxs(uint64_t v, float c) {
-  uint64_t r;
-  asm("{.reg .f32 a, b;\n\tmov.b64 {a, b}, %1;\n\tmax.f32 a, a, %2;\n\tmax.f32 b, b, %2;\n\tmov.b64 %0, {a, b};}"
-      : "=l"(r) : "l"(v), "f"(c));
-  return r;
+// 16 row partials per lane -> lanes 2r, 2r + 1 hold the total of row r in v[0] (transposed
+// butterfly: 8 + 4 + 2 + 1 exchanges, then xor 1)
+__device__ __forceinline__ void rows_reduce16(float (&v)[16]) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float a[8], b4[4], b2[2], b1;
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float send = hi ? v[k] : v[8 + k], keep = hi ? v[8 + k] : v[k];
+      a[k] = keep + __shfl_xor_sync(F, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float send = hi ? a[k] : a[4 + k], keep = hi ? a[4 + k] : a[k];
+      b4[k] = keep + __shfl_xor_sync(F, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float send = hi ? b4[k] : b4[2 + k], keep = hi ? b4[2 + k] : b4[k];
+      b2[k] = keep + __shfl_xor_sync(F, send, 4);
+    }
+  }
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? b2[0] : b2[1], keep = hi ? b2[1] : b2[0];
+    b1 = keep + __shfl_xor_sync(F, send, 2);
+  }
+  b1 += __shfl_xor_sync(F, b1, 1);
+  v[0] = b1;   // row 8 bit4 + 4 bit3 + 2 bit2 + bit1 of the lane
 }
 
-// The Y register tile of a lane: rows 16 w + r (r < 16) x columns 4 l + e (e < 4), packed as row
-// pairs y[q][e] = (row 2q, row 2q + 1) of column e, so that the per-row terms of P1 pair up for the
-// fp32x2 pipe and the row sums come out as pairs.
-using Tile = uint64_t[kPQ][4];
-__device__ __forceinline__ float yget(const Tile& y, int r, int e) {
-  return (r & 1) ? f2hi(y[r >> 1][e]) : f2lo(y[r >> 1][e]);
-}
-__device__ __forceinline__ void yset(Tile& y, int r, int e, float v) {
-  y[r >> 1][e] = (r & 1) ? f2pk(f2lo(y[r >> 1][e]), v) : f2pk(v, f2hi(y[r >> 1][e]));
-}
+// element e (0..3) of a lane's 4 consecutive columns held as two float2 pairs
+__device__ __forceinline__ float& el(float2 (&v)[2], int e) { return (e & 1) ? v[e >> 1].y : v[e >> 1].x; }
+__device__ __forceinline__ float elc(const float2 (&v)[2], int e) { return (e & 1) ? v[e >> 1].y : v[e >> 1].x; }
 
 // digits of 4 consecutive values of row `row` (s21 = 2^(21 - e)) into a global operand image
 __device__ __forceinline__ void store_digits(int8_t* img, int row, int col0, const float (&v)[4], float s21) {
@@ -352,13 +345,13 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       store_digits(xdig, i, 4 * lane, v, exp2i(21 - e));
     }
     // Y register tile (slack state; the X block is overwritten by the first product)
-    Tile y;
+    float2 y[kPR][2];
 #pragma unroll
     for (int r = 0; r < kPR; ++r)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = sw * kPR + r, j = 4 * lane + e;
-        yset(y, r, e, (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f);
+        el(y[r], e) = (p.Y && i < m && j < m) ? p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] : 0.f;
       }
     asm volatile("fence.proxy.async.global;" ::: "memory");   // X digits: generic -> async proxy
     slot_sync(slot);
@@ -463,15 +456,13 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       for (int r = 0; r < kPR; ++r) {
         const int i = sw * kPR + r;
         if (kFull) {
-          if (r & 1) continue;
           const float4 g = *reinterpret_cast<const float4*>(&sm.G[i][4 * lane]);
-          const float4 h = *reinterpret_cast<const float4*>(&sm.G[i + 1][4 * lane]);
-          y[r >> 1][0] = f2pk(g.x, h.x); y[r >> 1][1] = f2pk(g.y, h.y);
-          y[r >> 1][2] = f2pk(g.z, h.z); y[r >> 1][3] = f2pk(g.w, h.w);
+          y[r][0] = make_float2(g.x, g.y);
+          y[r][1] = make_float2(g.z, g.w);
         } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (i < n && 4 * lane + e < np) yset(y, r, e, sm.G[i][4 * lane + e]);
+            if (i < n && 4 * lane + e < np) el(y[r], e) = sm.G[i][4 * lane + e];
         }
       }
       slot_sync(slot);   // staging read, accumulators drained: hand the product resources over
@@ -484,64 +475,29 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       SSP(1);
 
       // ================= projection loop (P1 + P2 per sweep; slot-local) ======================
-      // Per sweep: the update and the sums of its output on the packed fp32x2 pipe (row pairs);
-      // each lane's 16 row partials transposed through shared memory (4 vector stores, 16 loads:
-      // lanes 2r, 2r + 1 each add 16 lanes' partials of row r, then one exchange), published with
-      // the warp's column partials and its share of sigma; slot barrier; 4 warps combine the column
-      // partials (one thread per column); slot barrier.
-      //
-      // Shifted column frame (kFull, every sweep after the first of an outer iteration). P1 adds
-      // t_i + v_j = (1 + sigma/m - r_i - c_j)/m; split as tau_i = (1 - r_i)/m and
-      // kappa_j = (sigma/m - c_j)/m, the column part is carried in a per-column offset V_j (the
-      // lane's 4 columns, nV = -V) instead of being added to each element: the tile holds
-      // s = y - V_j, the update is s' = max(s + tau_i, -V'_j) with V'_j = V_j + kappa_j (one packed add
-      // and the clamp per element instead of two adds and the clamp), and y = s + V_j again after
-      // the last sweep. The sums use s: column partials add 16 V_j per warp; row partials omit
-      // sum_j V_j, and sigma (their total) then omits m sum_j V_j, so the omitted terms cancel
-      // exactly in tau_i + kappa_j = (1 + sigma/m - r_i - c_j)/m. kappa_j ~ (column excess)/m stays
-      // small after the first sweep (whose operand is the product, of size ~1e1: that sweep runs
-      // in the direct form), so s keeps y's precision.
+      // Per sweep: the update and the sums of its output on the packed fp32x2 pipe; each warp's
+      // 16 row sums by a transposed butterfly, published with its column partials; slot barrier;
+      // 4 warps combine the column partials (one thread per column); slot barrier.
       int buf = 0;
-      float nV[4] = {0.f, 0.f, 0.f, 0.f};
-      float* const rowp = ss.rowp[sw];
-      auto sums = [&](const Tile& yy) {
-        // column partials over the warp's 16 rows (pairs of rows, then the two halves)
-        float cpart[4];
+      auto sums = [&](const float2 (&yy)[kPR][2]) {
+        float rp[kPR];
+        float2 c01 = make_float2(0.f, 0.f), c23 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint64_t c = f2add(yy[0][e], yy[1][e]);
-#pragma unroll
-          for (int q = 2; q < kPQ; ++q) c = f2add(c, yy[q][e]);
-          const float ct = f2lo(c) + f2hi(c);
-          cpart[e] = kFull ? fmaf(-(float)kPR, nV[e], ct) : ct;
+        for (int r = 0; r < kPR; ++r) {
+          const float2 t = __fadd2_rn(yy[r][0], yy[r][1]);
+          rp[r] = t.x + t.y;
+          c01 = __fadd2_rn(c01, yy[r][0]);
+          c23 = __fadd2_rn(c23, yy[r][1]);
         }
-        // row partials over the lane's 4 columns, two rows per packed add
+        // the warp's share of sigma = 1^T Y 1: an independent reduction that overlaps the butterfly
+        float ws = 0.f;
 #pragma unroll
-        for (int k = 0; k < kPQ / 2; ++k) {
-          const uint64_t ra = f2add(f2add(yy[2 * k][0], yy[2 * k][1]), f2add(yy[2 * k][2], yy[2 * k][3]));
-          const uint64_t rb = f2add(f2add(yy[2 * k + 1][0], yy[2 * k + 1][1]), f2add(yy[2 * k + 1][2], yy[2 * k + 1][3]));
-          // rows 4k .. 4k + 3 of this lane: chunk k, stored at chunk k ^ ((lane >> 1) & 3) of the
-          // lane's 16 floats (conflict-free 128-bit stores and scalar loads)
-          *reinterpret_cast<float4*>(rowp + lane * kPR + 4 * (k ^ ((lane >> 1) & 3))) =
-              make_float4(f2lo(ra), f2hi(ra), f2lo(rb), f2hi(rb));
-        }
-        __syncwarp();
-        float ph;
-        {
-          const int r = lane >> 1, h = lane & 1;
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int L = 16 * h + ((k + h) & 15);   // the two halves start on opposite bank halves
-            acc[k & 3] += rowp[L * kPR + 4 * ((r >> 2) ^ ((L >> 1) & 3)) + (r & 3)];
-          }
-          ph = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-        const float rt = ph + __shfl_xor_sync(0xffffffffu, ph, 1);   // row (lane >> 1) of the warp
-        const float ws = warp_sum(ph);                                // the warp's share of sigma
-        if ((lane & 1) == 0) ss.rsum[buf][sw][lane >> 1] = rt;
+        for (int r = 0; r < kPR; ++r) ws += rp[r];
+        ws = warp_sum(ws);
+        rows_reduce16(rp);
+        if ((lane & 1) == 0) ss.rsum[buf][sw][lane >> 1] = rp[0];
         if (lane == 0) ss.wsig[buf][sw] = ws;
-        *reinterpret_cast<float4*>(&ss.colp[buf][sw][4 * lane]) = make_float4(cpart[0], cpart[1], cpart[2], cpart[3]);
+        *reinterpret_cast<float4*>(&ss.colp[buf][sw][4 * lane]) = make_float4(c01.x, c01.y, c23.x, c23.y);
       };
       sums(y);
       if (lane == 0) ss.dl[buf][sw] = 0.f;
@@ -549,7 +505,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       int s = 0;
       float delta = 0.f;
       for (;;) {
-#ifndef FPFP_SS_ONE_BAR
+#ifndef FPFP_SS_PER_LANE_COMBINE   // (the per-lane variant below measured no faster: 7.36 vs 7.5 M)
         if (st < kS) {   // the kPW warp partials of column st (conflict-free rows)
           float c0 = 0.f, c1 = 0.f;
 #pragma unroll
@@ -561,76 +517,54 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         }
         slot_sync(slot);
         const float4 cs4 = *reinterpret_cast<const float4*>(&ss.csum[4 * lane]);
-        const float cs[4] = {cs4.x, cs4.y, cs4.z, cs4.w};
 #else
-        // every lane combines the warp partials of its own 4 columns (the same order as the
-        // one-thread-per-column combine, so the same sums): one slot barrier per sweep
-        float cs[4];
+        // every lane combines the kPW warp partials of its own 4 columns (8 vector loads, in the
+        // fixed warp order): one slot barrier per sweep instead of two
+        float4 cs4;
         {
-          const uint64_t* cp = reinterpret_cast<const uint64_t*>(&ss.colp[buf][0][4 * lane]);
-          uint64_t e0 = cp[0], o0 = cp[kS / 2], e1 = cp[1], o1 = cp[kS / 2 + 1];
+          float2 c01 = make_float2(0.f, 0.f), c23 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int w = 2; w < kPW; w += 2) {
-            e0 = f2add(e0, cp[w * (kS / 2)]);
-            e1 = f2add(e1, cp[w * (kS / 2) + 1]);
-            o0 = f2add(o0, cp[(w + 1) * (kS / 2)]);
-            o1 = f2add(o1, cp[(w + 1) * (kS / 2) + 1]);
+          for (int w = 0; w < kPW; ++w) {
+            const float4 v = *reinterpret_cast<const float4*>(&ss.colp[buf][w][4 * lane]);
+            c01 = __fadd2_rn(c01, make_float2(v.x, v.y));
+            c23 = __fadd2_rn(c23, make_float2(v.z, v.w));
           }
-          const uint64_t c01 = f2add(e0, o0), c23 = f2add(e1, o1);
-          cs[0] = f2lo(c01); cs[1] = f2hi(c01); cs[2] = f2lo(c23); cs[3] = f2hi(c23);
+          cs4 = make_float4(c01.x, c01.y, c23.x, c23.y);
         }
 #endif
-        const uint64_t* r2 = reinterpret_cast<const uint64_t*>(&ss.rsum[buf][sw][0]);   // row pairs
+        float rsr[kPR];
+#pragma unroll
+        for (int q = 0; q < kPR; q += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(&ss.rsum[buf][sw][q]);
+          rsr[q] = v.x; rsr[q + 1] = v.y; rsr[q + 2] = v.z; rsr[q + 3] = v.w;
+        }
         const float4 sg0 = *reinterpret_cast<const float4*>(&ss.wsig[buf][0]);
         const float4 sg1 = *reinterpret_cast<const float4*>(&ss.wsig[buf][4]);
         const float sigma = ((sg0.x + sg0.y) + (sg0.z + sg0.w)) + ((sg1.x + sg1.y) + (sg1.z + sg1.w));
-        const uint64_t ninv2 = f2pk(-inv_m, -inv_m);
+        const float tconst = (1.0f + sigma * inv_m) * inv_m;
+        const float2 inv2 = make_float2(-inv_m, -inv_m);
+        const float2 ncu01 = __fmul2_rn(make_float2(cs4.x, cs4.y), inv2);   // -c_j / m
+        const float2 ncu23 = __fmul2_rn(make_float2(cs4.z, cs4.w), inv2);
         buf ^= 1;
         float dmax = 0.f;
-        if (!kFull || s == 0) {   // direct form: z = max((y + t_i) - c_j/m, 0)
-          const float tconst = (1.0f + sigma * inv_m) * inv_m;
-          const uint64_t tc2 = f2pk(tconst, tconst);
-          uint64_t u2[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) u2[e] = f2pk(-cs[e] * inv_m, -cs[e] * inv_m);
+        for (int r = 0; r < kPR; ++r) {
+          const int i = sw * kPR + r;
+          const float ti = tconst - rsr[r] * inv_m;
+          const float2 t2 = make_float2(ti, ti);
 #pragma unroll
-          for (int q = 0; q < kPQ; ++q) {
-            const uint64_t t2 = f2fma(r2[q], ninv2, tc2);                      // t_i of rows 2q, 2q + 1
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint64_t yo = y[q][e];
-              uint64_t z = f2maxs(f2add(f2add(yo, t2), u2[e]), 0.f);            // P1, P2
-              if (!kFull) {
-                const int i = sw * kPR + 2 * q, j = 4 * lane + e;
-                z = f2pk((i < m && j < m) ? f2lo(z) : 0.f, (i + 1 < m && j < m) ? f2hi(z) : 0.f);
-              }
-              if (kDelta)
-                dmax = fmaxf(dmax, fmaxf(fabsf(f2lo(z) - f2lo(yo)), fabsf(f2hi(z) - f2hi(yo))));
-              y[q][e] = z;
+          for (int h = 0; h < 2; ++h) {
+            const float2 yo = y[r][h];
+            float2 z = __fadd2_rn(__fadd2_rn(yo, t2), h ? ncu23 : ncu01);    // P1: (y + t_i) - c_j/m
+            z.x = fmaxf(z.x, 0.f);                                            // P2
+            z.y = fmaxf(z.y, 0.f);
+            if (!kFull) {
+              const int j = 4 * lane + 2 * h;
+              if (!(i < m && j < m)) z.x = 0.f;
+              if (!(i < m && j + 1 < m)) z.y = 0.f;
             }
-          }
-        } else {                  // shifted column frame (see above)
-          const uint64_t tau0 = f2pk(inv_m, inv_m);
-          const float sg = sigma * inv_m * inv_m;
-          float kap[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            kap[e] = fmaf(cs[e], -inv_m, sg);                                 // kappa_j
-            nV[e] -= kap[e];
-          }
-#pragma unroll
-          for (int q = 0; q < kPQ; ++q) {
-            const uint64_t t2 = f2fma(r2[q], ninv2, tau0);                     // tau_i = (1 - r_i)/m
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint64_t yo = y[q][e];
-              const uint64_t z = f2maxs(f2add(yo, t2), nV[e]);                 // P1 + P2
-              if (kDelta) {   // (z + V') - (y + V) = (z - y) + kappa_j
-                const uint64_t dz = f2add(f2fma(yo, f2pk(-1.f, -1.f), z), f2pk(kap[e], kap[e]));
-                dmax = fmaxf(dmax, fmaxf(fabsf(f2lo(dz)), fabsf(f2hi(dz))));
-              }
-              y[q][e] = z;
-            }
+            if (kDelta) dmax = fmaxf(dmax, fmaxf(fabsf(z.x - yo.x), fabsf(z.y - yo.y)));
+            y[r][h] = z;
           }
         }
         sums(y);
@@ -646,14 +580,6 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         }
         ++s;
         if (delta < p.eps2 || s >= p.max_iter2) break;
-      }
-      if (kFull && s > 1) {   // back to the tile's own values: y = s + V_j (clamped entries: exactly 0)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint64_t v2 = f2pk(-nV[e], -nV[e]);
-#pragma unroll
-          for (int q = 0; q < kPQ; ++q) y[q][e] = f2add(y[q][e], v2);
-        }
       }
       total_sweeps += s;
       SSP(2);
@@ -679,10 +605,9 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int r = 4 * c + q;
-            const float xo[4] = {xa[q].x, xa[q].y, xa[q].z, xa[q].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) yset(y, r, e, fmaf(a2.x, yget(y, r, e), b2.x * xo[e]));
-            rmx[r] = fmaxf(fmaxf(yget(y, r, 0), yget(y, r, 1)), fmaxf(yget(y, r, 2), yget(y, r, 3)));
+            y[r][0] = __ffma2_rn(a2, y[r][0], __fmul2_rn(b2, make_float2(xa[q].x, xa[q].y)));
+            y[r][1] = __ffma2_rn(a2, y[r][1], __fmul2_rn(b2, make_float2(xa[q].z, xa[q].w)));
+            rmx[r] = fmaxf(fmaxf(y[r][0].x, y[r][0].y), fmaxf(y[r][1].x, y[r][1].y));
           }
           if (c + 1 < kPR / 4) {
 #pragma unroll
@@ -699,8 +624,8 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
             const int j = 4 * lane + e;
             if (i < n && j < np) {
               const float xo = __ldcg(X + (int64_t)i * np + j);
-              yset(y, r, e, fmaf(p.alpha, yget(y, r, e), (1.0f - p.alpha) * xo));
-              rmx[r] = fmaxf(rmx[r], yget(y, r, e));
+              el(y[r], e) = fmaf(p.alpha, el(y[r], e), (1.0f - p.alpha) * xo);
+              rmx[r] = fmaxf(rmx[r], el(y[r], e));
             }
           }
         }
@@ -723,9 +648,6 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       // DESIGN.md §6), rho, and the digits of the new X for the next GEMM1 (row scale from the row
       // max of X~: rounding and the division are monotonic, so it is the max of the stored row)
       const float inv_scale = p.rescale ? 1.0f / mu : 1.0f;
-      // rho decides only the outer stop test (eps1 > 0) and the reported last value: with eps1 <= 0
-      // (fixed outer counts) only the call's last iteration re-reads the old X for it
-      const bool want_rho = p.eps1 > 0.f || it + 1 >= p.max_iter1;
       float rl = 0.f;
       auto finish_row = [&](int r, const float (&xn)[4]) {
         const int i = sw * kPR + r;
@@ -733,16 +655,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
         if (lane == 0) ss.xscale[i] = pow2(e - 14);
         store_digits(xdig, i, 4 * lane, xn, exp2i(21 - e));
       };
-      if (kFull && !want_rho) {
-#pragma unroll
-        for (int r = 0; r < kPR; ++r) {
-          float xn[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) xn[e] = yget(y, r, e) * inv_scale;
-          __stcg(reinterpret_cast<float4*>(const_cast<float*>(xrow0) + r * kS), make_float4(xn[0], xn[1], xn[2], xn[3]));
-          finish_row(r, xn);
-        }
-      } else if (kFull) {
+      if (kFull) {
         float4 xa[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) xa[q] = __ldcg(reinterpret_cast<const float4*>(xrow0 + q * kS));   // kFull: np = kS
@@ -759,7 +672,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
             const int r = 4 * c + q;
             float xn[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) xn[e] = yget(y, r, e) * inv_scale;
+            for (int e = 0; e < 4; ++e) xn[e] = elc(y[r], e) * inv_scale;
             rl = fmaxf(rl, fmaxf(fmaxf(fabsf(xn[0] - xa[q].x), fabsf(xn[1] - xa[q].y)),
                                  fmaxf(fabsf(xn[2] - xa[q].z), fabsf(xn[3] - xa[q].w))));
             __stcg(reinterpret_cast<float4*>(const_cast<float*>(xrow0) + r * kS),
@@ -779,7 +692,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int j = 4 * lane + e;
-            xn[e] = yget(y, r, e) * inv_scale;
+            xn[e] = elc(y[r], e) * inv_scale;
             if (i < n && j < np) {
               const float xo = __ldcg(X + (int64_t)i * np + j);
               rl = fmaxf(rl, fabsf(xn[e] - xo));
@@ -793,15 +706,13 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
       }
       SSP(4);
       asm volatile("fence.proxy.async.global;" ::: "memory");   // X digits: generic -> async proxy
-      if (want_rho) {
-        rl = warp_max(rl);
-        if (lane == 0) ss.red[sw] = rl;
-        slot_sync(slot);
-        rho = 0.f;
+      rl = warp_max(rl);
+      if (lane == 0) ss.red[sw] = rl;
+      slot_sync(slot);
+      rho = 0.f;
 #pragma unroll
-        for (int w = 0; w < kPW; ++w) rho = fmaxf(rho, ss.red[w]);
-        slot_sync(slot);
-      }
+      for (int w = 0; w < kPW; ++w) rho = fmaxf(rho, ss.red[w]);
+      slot_sync(slot);
       ++it;
       SSP(5);
       if (rho < p.eps1) { conv = 1; break; }
@@ -821,7 +732,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int i = sw * kPR + r, j = 4 * lane + e;
-          if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = yget(y, r, e);
+          if (i < m && j < m) p.Y[(int64_t)pair * m * m + (int64_t)i * m + j] = el(y[r], e);
         }
     }
     if (st == 0) {
