@@ -552,7 +552,7 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   plan_projection(h);
   A(alloc_arr(h->rowpart, (size_t)h->CB * h->yrows));
   A(alloc_arr(h->colpart, (size_t)h->RB * M));
-  A(alloc_arr(h->r, h->yrows)); A(alloc_arr(h->c, (size_t)M + 1));
+  A(alloc_arr(h->r, 2 * h->yrows)); A(alloc_arr(h->c, 2 * ((size_t)M + 1)));   // two generations (replay)
   A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
@@ -1086,6 +1086,7 @@ int fastpfp_iterate(fastpfp_handle* h, double alpha, double lambda, double eps1,
         CK(h, cudaMemsetAsync(h->xrowmax, 0, (size_t)N * sizeof(unsigned long long), s));
       }
       pa.tile_ctr = h->tile_ctr;
+      pa.replay = proj_replay_default();
       CK(h, cudaMemsetAsync(h->tile_ctr, 0, sizeof(unsigned), s));
       CK(h, launch_proj(pa, h->grid, s));
       h->stats.launches += 1;
@@ -1256,7 +1257,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
   auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
   A(alloc_buf(Yp, (int)m, (int)m));
   A(alloc_arr(tmp.rowpart, (size_t)tmp.CB * m)); A(alloc_arr(tmp.colpart, (size_t)tmp.RB * m));
-  A(alloc_arr(tmp.r, m)); A(alloc_arr(tmp.c, m + 1));
+  A(alloc_arr(tmp.r, 2 * m)); A(alloc_arr(tmp.c, 2 * (m + 1)));
   A(alloc_arr(tmp.sig_part, tmp.grid)); A(alloc_arr(tmp.mu_part, tmp.grid));
   A(alloc_arr(tmp.dlt_part, tmp.grid)); A(alloc_arr(tmp.rho_part, tmp.grid));
   A(alloc_arr(tmp.iters, 1)); A(alloc_arr(tmp.done, 1));
@@ -1270,6 +1271,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
     pa.rowpart = tmp.rowpart; pa.colpart = tmp.colpart; pa.r = tmp.r; pa.c = tmp.c;
     pa.sig_part = tmp.sig_part; pa.dlt_part = tmp.dlt_part; pa.mu_part = tmp.mu_part;
     pa.rho_part = tmp.rho_part; pa.iter_out = tmp.iters; pa.done = tmp.done;
+    pa.replay = proj_replay_default();
     A(launch_proj(pa, tmp.grid, s));
     A(download(Yp, Y, 1, s));
     A(cudaMemcpyAsync(&it, tmp.iters, sizeof(DevIter), cudaMemcpyDeviceToHost, s));

@@ -142,7 +142,13 @@ struct ProjArgs {
   // the pass's grid barrier shrinks; results do not depend on which block ran a tile (partials are
   // indexed by tile). nullptr: static schedule.
   unsigned* tile_ctr;
+  // kProjFull, single GPU: checkpointed sweeps (proj.cu replay_pass): Y stored every other sweep,
+  // the sweeps after the first re-applied from the last stored Y in fp32. r and c then hold two
+  // generations ([2][rows] and [2][m + 1]).
+  int replay;
 };
+// default of ProjArgs::replay (environment FPFP_PROJ_REPLAY=0 turns it off: experiments / A-B)
+int proj_replay_default();
 
 constexpr int kProjThreads = 256;
 #ifndef FPFP_PROJ_TC

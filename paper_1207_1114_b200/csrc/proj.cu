@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -308,6 +309,199 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   __syncthreads();
 }
 
+#if FPFP_PROJ_BULK
+// Replay pass (single GPU, p.replay; DESIGN.md §8 "checkpointed sweeps"). Sweep k's output is an
+// elementwise function of an earlier stored Y and the correction vectors of the sweeps between:
+// Z_k = max(Z_{k-1} + t^(k) - u^(k), 0) with t^(k), u^(k) from the sums of Z_{k-1}. So the inner
+// loop stores Y only every other sweep: pass k reads the last stored Y (the checkpoint) and
+// re-applies D = 1 or 2 sweeps in registers; it writes Z_k only when asked (`write`: the odd sweeps
+// and the cap's last), and always emits the sums of Z_k and delta = max|Z_k - Z_{k-1}| like
+// tile_pass. Per 2 sweeps: 2 reads + 1 write of Y instead of 2 reads + 2 writes. These sweeps follow
+// the first of the outer iteration (the fp64 one, whose operand is the product), so their
+// correction runs in fp32, as in the on-chip kernel: t_i = fl32(tconst - r_i/m),
+// u_j = fl32(c_j/m), z = max(fl32(fl32(y + t_i) - u_j), 0). A re-applied sweep repeats the same
+// fp32 operations on the same stored operand, so every pass sees the same Z values.
+//   rs[d], cs[d], tc[d]: row sums, column sums and tconst = (1 + sigma/m)/m of the sums each
+//   re-applied sweep d < D consumes (d = D - 1: this pass's sweep).
+template <bool kFull, bool kMu>
+__device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, bool write,
+                                            const double* const (&rs)[2], const double* const (&cs)[2],
+                                            const double (&tc)[2], float& dmax, ProjSmem& sm, Ring& ring_st,
+                                            double* mu_acc) {
+  const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = rb * p.TR;
+  const int row1 = min(p.rows, row0 + p.TR);
+  const int colbase = cb * kProjTC;
+  const double inv_m = 1.0 / (double)p.m;
+
+  float u[2][kQ][4], colf[kQ][4];
+  bool inrow[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int j0 = colbase + q * 128 + lane * 4;
+    inrow[q] = kFull || j0 < p.ldY;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = j0 + e;
+      const bool v = kFull || j < p.m;
+#pragma unroll
+      for (int d = 0; d < 2; ++d) u[d][q][e] = (v && d < D) ? (float)(__ldcg(cs[d] + j) * inv_m) : 0.0f;
+      colf[q][e] = 0.0f;
+    }
+  }
+  double r_lo[2], r_hi[2];
+  {
+    const int ia = row0 + warp + kWarps * lane, ib = ia + kWarps * 32;
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      r_lo[d] = (d < D && ia < row1) ? __ldcg(rs[d] + ia) : 0.0;
+      r_hi[d] = (d < D && ib < row1) ? __ldcg(rs[d] + ib) : 0.0;
+    }
+  }
+
+  const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
+  float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
+  uint64_t* wbar = ring_st.bar + warp * kSlots;
+  const uint32_t seq0 = ring_st.seq;
+  const int i0 = row0 + warp;
+  const int nrows_w = i0 < row1 ? (row1 - i0 + kWarps - 1) / kWarps : 0;
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < kSlots && k < nrows_w; ++k) {
+      const uint32_t slot = (seq0 + k) % kSlots;
+      ring_issue(wbar + slot, wbuf + slot * kProjTC, p.Y + (int64_t)(i0 + k * kWarps) * p.ldY + colbase,
+                 row_bytes);
+    }
+  }
+  __syncwarp();
+  for (int tg = 0; tg < nrows_w; tg += 4) {
+    double rq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u4 = 0; u4 < 4; ++u4) {
+      const int t = tg + u4;
+      if (t >= nrows_w) break;
+      const int i = i0 + t * kWarps;
+      const uint32_t slot = (seq0 + t) % kSlots;
+      ring_wait(wbar + slot, ((seq0 + t) / kSlots) & 1u);
+      float4 cur[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        cur[q] = inrow[q] ? *reinterpret_cast<const float4*>(wbuf + slot * kProjTC + q * 128 + lane * 4)
+                          : make_float4(0, 0, 0, 0);
+      __syncwarp();
+      if (lane == 0 && t + kSlots < nrows_w) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        ring_issue(wbar + slot, wbuf + slot * kProjTC, p.Y + (int64_t)(i + kSlots * kWarps) * p.ldY + colbase,
+                   row_bytes);
+      }
+      float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
+      float tf[2];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const double rlo = __shfl_sync(0xffffffffu, r_lo[d], t & 31);
+        const double rhi = __shfl_sync(0xffffffffu, r_hi[d], t & 31);
+        tf[d] = (float)(tc[d] - (t < 32 ? rlo : rhi) * inv_m);
+      }
+      float racc_f = 0.0f;
+      float4 xq[kQ];
+      const bool xrow = kMu && i < p.n;
+      if (kMu) {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int j0 = colbase + q * 128 + lane * 4;
+          xq[q] = (xrow && j0 < p.np) ? __ldcs(reinterpret_cast<const float4*>(p.X + (int64_t)i * p.ldX + j0))
+                                      : make_float4(0, 0, 0, 0);
+        }
+      }
+      double xrmax = 0.0;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        float* ve = reinterpret_cast<float*>(&cur[q]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = colbase + q * 128 + lane * 4 + e;
+          const bool valid = kFull || j < p.m;
+          float zp = ve[e];
+          float z = fmaxf((zp + tf[0]) - u[0][q][e], 0.0f);   // P1 + P2 (fp32)
+          if (D > 1) {
+            zp = z;
+            z = fmaxf((zp + tf[1]) - u[1][q][e], 0.0f);
+          }
+          if (!valid) {   // outside m: stays 0 (delta as tile_pass: against the stored value)
+            z = 0.0f;
+            zp = ve[e];
+          }
+          dmax = fmaxf(dmax, fabsf(z - zp));                   // delta
+          ve[e] = z;
+          racc_f += z;
+          colf[q][e] += z;
+          if (kMu && xrow && j < p.np) {
+            const double xt = blend_xt(p.alpha, 1.0 - p.alpha, reinterpret_cast<const float*>(&xq[q])[e], z);
+            *mu_acc = fmax(*mu_acc, xt);
+            xrmax = fmax(xrmax, fabs(xt));
+          }
+        }
+      }
+      if (kMu && p.xrowmax) {
+        const double v = warp_max(xrmax);
+        if (lane == 0 && xrow) atomicMax(p.xrowmax + i, (unsigned long long)__double_as_longlong(v));
+      }
+      if (write) {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          if (inrow[q]) __stcg(reinterpret_cast<float4*>(rowp + q * 128), cur[q]);
+      }
+      rq[u4] = (double)racc_f;
+    }
+    const bool b4 = lane & 16, b3 = lane & 8;
+    double k0 = b4 ? rq[2] : rq[0], k1 = b4 ? rq[3] : rq[1];
+    k0 += __shfl_xor_sync(0xffffffffu, b4 ? rq[0] : rq[2], 16);
+    k1 += __shfl_xor_sync(0xffffffffu, b4 ? rq[1] : rq[3], 16);
+    double k = b3 ? k1 : k0;
+    k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    const int rsel = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+    if ((lane & 7) == 0 && tg + rsel < nrows_w)
+      p.rowpart[(int64_t)cb * p.rows + i0 + (tg + rsel) * kWarps] = k;
+  }
+  ring_st.seq = seq0 + (uint32_t)nrows_w;
+#pragma unroll
+  for (int q = 0; q < kQ; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sm.col[warp][q * 128 + lane * 4 + e] = (double)colf[q][e];
+  __syncthreads();
+  for (int jj = threadIdx.x; jj < kProjTC; jj += kProjThreads) {
+    const int j = colbase + jj;
+    if (j < p.m) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += sm.col[w][jj];
+      p.colpart[(int64_t)rb * p.m + j] = s;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void replay_tile(const ProjArgs& p, int t, int D, bool write, bool mu_fused,
+                                            const double* const (&rs)[2], const double* const (&cs)[2],
+                                            const double (&tc)[2], float& dmax, ProjSmem& sm, Ring& ring,
+                                            double& mu) {
+  const int rb = t / p.CB, cb = t - rb * p.CB;
+  const bool full = (cb + 1) * kProjTC <= p.m;
+  if (mu_fused && rb * p.TR < p.n && cb * kProjTC < p.np) {
+    if (full) replay_pass<true, true>(p, t, D, write, rs, cs, tc, dmax, sm, ring, &mu);
+    else replay_pass<false, true>(p, t, D, write, rs, cs, tc, dmax, sm, ring, &mu);
+  } else {
+    if (full) replay_pass<true, false>(p, t, D, write, rs, cs, tc, dmax, sm, ring, nullptr);
+    else replay_pass<false, false>(p, t, D, write, rs, cs, tc, dmax, sm, ring, nullptr);
+  }
+}
+#endif
+
 // one sweep over a tile: the bounds-free variant when all 512 columns are inside m
 __device__ __forceinline__ void sweep_tile(const ProjArgs& p, int t, double sigma, float& dmax,
                                            ProjSmem& sm, Ring& ring) {
@@ -327,7 +521,10 @@ __device__ __forceinline__ void sweep_tile_mu(const ProjArgs& p, int t, double s
 // r_i = sum_cb rowpart[cb][i], c_j = sum_rb colpart[rb][j]; one warp per index: lane l sums the
 // partials l, l+32, ... and an xor tree combines the lanes (a fixed order => deterministic).
 // Per-block partial of sigma = sum of the c_j this block produced (fixed assignment of j to blocks).
-__device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
+__device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm, double* r_out = nullptr,
+                                             double* c_out = nullptr) {
+  if (!r_out) r_out = p.r;
+  if (!c_out) c_out = p.c;
   // one thread per column / row, partials summed in block order (coalesced across threads,
   // independent loads in flight; fixed order => deterministic)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -344,7 +541,7 @@ __device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
     }
     for (; rb < p.RB; ++rb) s0 += __ldcg(p.colpart + (int64_t)rb * p.m + j);
     const double s = (s0 + s1) + (s2 + s3);
-    p.c[j] = s;
+    c_out[j] = s;
     local += s;
   }
   for (int i = gt; i < p.rows; i += nt) {
@@ -357,7 +554,7 @@ __device__ __forceinline__ void reduce_phase(const ProjArgs& p, ProjSmem& sm) {
       s3 += __ldcg(p.rowpart + (int64_t)(cb + 3) * p.rows + i);
     }
     for (; cb < p.CB; ++cb) s0 += __ldcg(p.rowpart + (int64_t)cb * p.rows + i);
-    p.r[i] = (s0 + s1) + (s2 + s3);
+    r_out[i] = (s0 + s1) + (s2 + s3);
   }
   local = warp_sum(local);
   if (lane == 0) sm.red[warp] = local;
@@ -650,6 +847,16 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
   float delta = 0.0f;
   bool mu_fused = false;
   double mu_loc = -INFINITY;
+  // checkpointed sweeps (replay_pass): the sums of generation g (of Z_g) live in buffer g & 1
+#if FPFP_PROJ_BULK
+  const bool replay = p.replay != 0;
+#else
+  const bool replay = false;
+#endif
+  double* const rbuf[2] = {p.r, p.r + p.rows};
+  double* const cbuf[2] = {p.c, p.c + p.m + 1};
+  double sig[2] = {sigma, 0.0};
+  bool stored = true;   // Z of the last sweep is in Y
 #ifdef FPFP_PROJ_PROF
   unsigned long long pt[4] = {0, 0, 0, 0}, tmin = ~0ull, tmax = 0;
   auto gt = []() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
@@ -657,12 +864,29 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 #endif
   for (;;) {
     float dmax = 0.0f;
+    const int k = sweeps + 1;   // this sweep
     // the cap's last sweep is known in advance: it also reduces mu (the eps2 stop is not)
     mu_fused = p.do_finalize && sweeps + 1 >= p.max_iter2;
-    if (mu_fused) {
-      for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile_mu(p, t, sigma, dmax, sm, ring, mu_loc); });
+    if (!replay || k == 1) {
+      if (mu_fused) {
+        for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile_mu(p, t, sigma, dmax, sm, ring, mu_loc); });
+      } else {
+        for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile(p, t, sigma, dmax, sm, ring); });
+      }
     } else {
-      for_tiles(p, ntiles, pass++, &s_tile, [&](int t) { sweep_tile(p, t, sigma, dmax, sm, ring); });
+#if FPFP_PROJ_BULK
+      // even k: one sweep from the stored Z_{k-1}; odd k: two from the stored Z_{k-2}, stored
+      const int D = (k & 1) ? 2 : 1;
+      const bool write = (k & 1) || sweeps + 1 >= p.max_iter2;
+      const int g0 = k - D;   // generation of the checkpoint
+      const double* const rs[2] = {rbuf[g0 & 1], rbuf[(g0 + 1) & 1]};
+      const double* const cs[2] = {cbuf[g0 & 1], cbuf[(g0 + 1) & 1]};
+      const double inv_m = 1.0 / (double)p.m;
+      const double tc[2] = {(1.0 + sig[g0 & 1] * inv_m) * inv_m, (1.0 + sig[(g0 + 1) & 1] * inv_m) * inv_m};
+      for_tiles(p, ntiles, pass++, &s_tile,
+                [&](int t) { replay_tile(p, t, D, write, mu_fused, rs, cs, tc, dmax, sm, ring, mu_loc); });
+      stored = write;
+#endif
     }
     dmax = block_max(dmax, sm, 0.0f);
     if (threadIdx.x == 0) p.dlt_part[blockIdx.x] = dmax;
@@ -673,12 +897,14 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[1] += t - tq; tq = t; }
 #endif
-    reduce_phase(p, sm);
+    if (replay) reduce_phase(p, sm, rbuf[k & 1], cbuf[k & 1]);
+    else reduce_phase(p, sm);
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[2] += t - tq; tq = t; }
 #endif
     grid.sync();
     sigma = grid_sigma(p, sm);
+    sig[k & 1] = sigma;
     delta = grid_max(p.dlt_part, sm, 0.0f);
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[3] += t - tq; tq = t; }
@@ -686,6 +912,19 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     ++sweeps;
     if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
   }
+#if FPFP_PROJ_BULK
+  if (!stored) {   // stopped on delta after a sweep that was not stored: store Z_k (k even)
+    const int k = sweeps;
+    const double* const rs[2] = {rbuf[(k - 1) & 1], rbuf[k & 1]};
+    const double* const cs[2] = {cbuf[(k - 1) & 1], cbuf[k & 1]};
+    const double inv_m = 1.0 / (double)p.m;
+    const double tc[2] = {(1.0 + sig[(k - 1) & 1] * inv_m) * inv_m, 0.0};
+    float dd = 0.0f;
+    for_tiles(p, ntiles, pass++, &s_tile,
+              [&](int t) { replay_tile(p, t, 1, true, false, rs, cs, tc, dd, sm, ring, mu_loc); });
+    grid.sync();
+  }
+#endif
 
 #ifdef FPFP_PROJ_PROF
   if ((blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x == 0)
@@ -826,6 +1065,14 @@ inline int grid_for(int64_t total) {
 }
 
 }  // namespace
+
+int proj_replay_default() {
+  static const int v = [] {
+    const char* e = getenv("FPFP_PROJ_REPLAY");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
 
 int proj_max_grid(int device) {
   int sms = 0, per_sm = 0;

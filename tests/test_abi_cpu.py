@@ -28,6 +28,18 @@ def test_library_exports_every_declared_symbol():
         assert f" T {s}" in out, s
 
 
+def test_library_links_completely():
+    # every symbol of the library's own namespace is defined inside it (a declaration left without
+    # a definition loads lazily here and fails only at the first call on the GPU box)
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    L = ctypes.CDLL(_native.LIB_PATH, mode=os.RTLD_NOW)
+    assert L is not None
+    out = subprocess.run(["nm", "-D", "--undefined-only", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "fpfp" not in out, [ln for ln in out.splitlines() if "fpfp" in ln]
+
+
 def test_library_is_sm100a_code():
     if not os.path.exists(_native.LIB_PATH):
         pytest.skip("library not built")

@@ -12,9 +12,10 @@ alpha = 0.5, 20 sweeps per outer iteration, eps = 0), in the launch configuratio
   FASTPFP_LOCKSTEP_OUT=<json path>.
 * `test_c5_full_size_sweep_sums`: the streaming projection computes the row/column sums of a sweep's
   output with fp32 per-lane partials (16 elements of a row, <= 64 rows of a column) and fp64 beyond
-  (DESIGN.md §6). Sweep 2 of a 2-sweep launch consumes those sums; it is compared with the oracle's
+  (DESIGN.md §6). Sweep 2 of a 2-sweep launch consumes those sums (and, as every sweep after the
+  first of an outer iteration, applies its correction in fp32); it is compared with the oracle's
   fp64 sweep (oracle.sweep = P2(P1(Y))) of the GPU's own sweep-1 output, within the
-  bound the fp32 partials allow. Nothing here comes from the CUDA path except the values under test.
+  bound the fp32 partials and the fp32 correction allow. Nothing here comes from the CUDA path except the values under test.
 """
 import json
 import os
@@ -122,10 +123,15 @@ def test_c5_full_size_sweep_sums(c5):
     sig = c.sum()
     u = 2.0**-24
     # fp32 partials: row sums over 16-element lane groups (<= 15 u r_i), column sums over <= 64
-    # rows (<= 63 u c_j), sigma from the column partials; fp64 rounding of the correction; the
-    # final rounding of Z to fp32 (<= u |Z|); x2 margin
+    # rows (<= 63 u c_j), sigma from the column partials. Sweeps after an outer iteration's first
+    # correct in fp32 (checkpointed sweeps): t_i and c_j/m rounded to fp32, then
+    # fl(fl(y + t_i) - c_j/m), whose two roundings are <= u (|y| + |t_i| + |c_j/m|) each; the result is
+    # stored as computed; x2 margin
+    t = (1.0 + sig / m - r) / m
+    uc = c / m
+    mag = np.abs(y1) + np.abs(t)[:, None] + uc[None, :]
     bound = 2.0 * ((16 * u * r[:, None] + 64 * u * c[None, :] + 64 * u * sig / m) / m
-                   + u * np.abs(Z) + 1e-15 * (np.abs(y1) + (r[:, None] + c[None, :]) / m + sig / m**2))
+                   + u * (np.abs(t)[:, None] + uc[None, :]) + 2 * u * mag + u * np.abs(Z))
     err = np.abs(y2.astype(np.float64) - Z)
     ratio = float(np.max(err / np.maximum(bound, 1e-300)))
     print(json.dumps({"max_abs_err": float(err.max()), "max_err_over_bound": ratio,
