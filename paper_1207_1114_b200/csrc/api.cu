@@ -552,7 +552,7 @@ static int create_impl(int64_t n_glob, int64_t n_prime, int64_t d, int rank, int
   plan_projection(h);
   A(alloc_arr(h->rowpart, (size_t)h->CB * h->yrows));
   A(alloc_arr(h->colpart, (size_t)h->RB * M));
-  A(alloc_arr(h->r, 2 * h->yrows)); A(alloc_arr(h->c, 2 * ((size_t)M + 1)));   // two generations (replay)
+  A(alloc_arr(h->r, kProjReplayC * h->yrows)); A(alloc_arr(h->c, kProjReplayC * ((size_t)M + 1)));   // replay generations
   A(alloc_arr(h->sig_part, h->grid)); A(alloc_arr(h->mu_part, h->grid));
   A(alloc_arr(h->dlt_part, h->grid)); A(alloc_arr(h->rho_part, h->grid));
   A(alloc_arr(h->iters, kMaxCheck)); A(alloc_arr(h->done, 1)); A(alloc_arr(h->flags, 1));
@@ -1257,7 +1257,7 @@ int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t
   auto A = [&](cudaError_t e) { if (e != cudaSuccess && rc == FASTPFP_OK) rc = FASTPFP_ECUDA; };
   A(alloc_buf(Yp, (int)m, (int)m));
   A(alloc_arr(tmp.rowpart, (size_t)tmp.CB * m)); A(alloc_arr(tmp.colpart, (size_t)tmp.RB * m));
-  A(alloc_arr(tmp.r, 2 * m)); A(alloc_arr(tmp.c, 2 * (m + 1)));
+  A(alloc_arr(tmp.r, kProjReplayC * m)); A(alloc_arr(tmp.c, kProjReplayC * (m + 1)));
   A(alloc_arr(tmp.sig_part, tmp.grid)); A(alloc_arr(tmp.mu_part, tmp.grid));
   A(alloc_arr(tmp.dlt_part, tmp.grid)); A(alloc_arr(tmp.rho_part, tmp.grid));
   A(alloc_arr(tmp.iters, 1)); A(alloc_arr(tmp.done, 1));

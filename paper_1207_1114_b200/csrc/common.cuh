@@ -144,9 +144,13 @@ struct ProjArgs {
   unsigned* tile_ctr;
   // kProjFull, single GPU: checkpointed sweeps (proj.cu replay_pass): Y stored every other sweep,
   // the sweeps after the first re-applied from the last stored Y in fp32. r and c then hold two
-  // generations ([2][rows] and [2][m + 1]).
+  // kProjReplayC generations ([kProjReplayC][rows] and [kProjReplayC][m + 1]).
   int replay;
 };
+#ifndef FPFP_PROJ_REPLAY_C
+#define FPFP_PROJ_REPLAY_C 2
+#endif
+constexpr int kProjReplayC = FPFP_PROJ_REPLAY_C;   // replay: Y stored every kProjReplayC sweeps
 // default of ProjArgs::replay (environment FPFP_PROJ_REPLAY=0 turns it off: experiments / A-B)
 int proj_replay_default();
 

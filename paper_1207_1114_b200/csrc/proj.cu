@@ -309,6 +309,8 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   __syncthreads();
 }
 
+constexpr int kRC = kProjReplayC;   // checkpoint interval: Y stored every kRC sweeps
+
 #if FPFP_PROJ_BULK
 // Replay pass (single GPU, p.replay; DESIGN.md §8 "checkpointed sweeps"). Sweep k's output is an
 // elementwise function of an earlier stored Y and the correction vectors of the sweeps between:
@@ -325,8 +327,8 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
 //   re-applied sweep d < D consumes (d = D - 1: this pass's sweep).
 template <bool kFull, bool kMu>
 __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, bool write,
-                                            const double* const (&rs)[2], const double* const (&cs)[2],
-                                            const double (&tc)[2], float& dmax, ProjSmem& sm, Ring& ring_st,
+                                            const double* const (&rs)[kRC], const double* const (&cs)[kRC],
+                                            const double (&tc)[kRC], float& dmax, ProjSmem& sm, Ring& ring_st,
                                             double* mu_acc) {
   const int rb = tile / p.CB, cb = tile - (tile / p.CB) * p.CB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -335,7 +337,7 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
   const int colbase = cb * kProjTC;
   const double inv_m = 1.0 / (double)p.m;
 
-  float u[2][kQ][4], colf[kQ][4];
+  float u[kRC][kQ][4], colf[kQ][4];
   bool inrow[kQ];
 #pragma unroll
   for (int q = 0; q < kQ; ++q) {
@@ -346,15 +348,15 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
       const int j = j0 + e;
       const bool v = kFull || j < p.m;
 #pragma unroll
-      for (int d = 0; d < 2; ++d) u[d][q][e] = (v && d < D) ? (float)(__ldcg(cs[d] + j) * inv_m) : 0.0f;
+      for (int d = 0; d < kRC; ++d) u[d][q][e] = (v && d < D) ? (float)(__ldcg(cs[d] + j) * inv_m) : 0.0f;
       colf[q][e] = 0.0f;
     }
   }
-  double r_lo[2], r_hi[2];
+  double r_lo[kRC], r_hi[kRC];
   {
     const int ia = row0 + warp + kWarps * lane, ib = ia + kWarps * 32;
 #pragma unroll
-    for (int d = 0; d < 2; ++d) {
+    for (int d = 0; d < kRC; ++d) {
       r_lo[d] = (d < D && ia < row1) ? __ldcg(rs[d] + ia) : 0.0;
       r_hi[d] = (d < D && ib < row1) ? __ldcg(rs[d] + ib) : 0.0;
     }
@@ -397,9 +399,9 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
                    row_bytes);
       }
       float* rowp = p.Y + (int64_t)i * p.ldY + colbase + lane * 4;
-      float tf[2];
+      float tf[kRC];
 #pragma unroll
-      for (int d = 0; d < 2; ++d) {
+      for (int d = 0; d < kRC; ++d) {
         const double rlo = __shfl_sync(0xffffffffu, r_lo[d], t & 31);
         const double rhi = __shfl_sync(0xffffffffu, r_hi[d], t & 31);
         tf[d] = (float)(tc[d] - (t < 32 ? rlo : rhi) * inv_m);
@@ -425,10 +427,12 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
           const bool valid = kFull || j < p.m;
           float zp = ve[e];
           float z = fmaxf((zp + tf[0]) - u[0][q][e], 0.0f);   // P1 + P2 (fp32)
-          if (D > 1) {
-            zp = z;
-            z = fmaxf((zp + tf[1]) - u[1][q][e], 0.0f);
-          }
+#pragma unroll
+          for (int d = 1; d < kRC; ++d)
+            if (d < D) {
+              zp = z;
+              z = fmaxf((zp + tf[d]) - u[d][q][e], 0.0f);
+            }
           if (!valid) {   // outside m: stays 0 (delta as tile_pass: against the stored value)
             z = 0.0f;
             zp = ve[e];
@@ -487,8 +491,8 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
 }
 
 __device__ __forceinline__ void replay_tile(const ProjArgs& p, int t, int D, bool write, bool mu_fused,
-                                            const double* const (&rs)[2], const double* const (&cs)[2],
-                                            const double (&tc)[2], float& dmax, ProjSmem& sm, Ring& ring,
+                                            const double* const (&rs)[kRC], const double* const (&cs)[kRC],
+                                            const double (&tc)[kRC], float& dmax, ProjSmem& sm, Ring& ring,
                                             double& mu) {
   const int rb = t / p.CB, cb = t - rb * p.CB;
   const bool full = (cb + 1) * kProjTC <= p.m;
@@ -853,9 +857,11 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 #else
   const bool replay = false;
 #endif
-  double* const rbuf[2] = {p.r, p.r + p.rows};
-  double* const cbuf[2] = {p.c, p.c + p.m + 1};
-  double sig[2] = {sigma, 0.0};
+  // generation g (the sums of Z_g) lives in slot g % kRC of r [kRC][rows], c [kRC][m + 1], sig
+  auto rbuf = [&](int g) { return p.r + (int64_t)(g % kRC) * p.rows; };
+  auto cbuf = [&](int g) { return p.c + (int64_t)(g % kRC) * (p.m + 1); };
+  double sig[kRC];
+  sig[0] = sigma;
   bool stored = true;   // Z of the last sweep is in Y
 #ifdef FPFP_PROJ_PROF
   unsigned long long pt[4] = {0, 0, 0, 0}, tmin = ~0ull, tmax = 0;
@@ -875,14 +881,22 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
       }
     } else {
 #if FPFP_PROJ_BULK
-      // even k: one sweep from the stored Z_{k-1}; odd k: two from the stored Z_{k-2}, stored
-      const int D = (k & 1) ? 2 : 1;
-      const bool write = (k & 1) || sweeps + 1 >= p.max_iter2;
+      // the stored checkpoints are Z_1, Z_{1+kRC}, Z_{1+2kRC}, ... and the cap's last sweep: sweep k
+      // re-applies D = k - (last checkpoint before k) sweeps and is stored when D == kRC
+      const int D = (k - 2) % kRC + 1;
+      const bool write = D == kRC || sweeps + 1 >= p.max_iter2;
       const int g0 = k - D;   // generation of the checkpoint
-      const double* const rs[2] = {rbuf[g0 & 1], rbuf[(g0 + 1) & 1]};
-      const double* const cs[2] = {cbuf[g0 & 1], cbuf[(g0 + 1) & 1]};
+      const double* rs[kRC];
+      const double* cs[kRC];
+      double tc[kRC];
       const double inv_m = 1.0 / (double)p.m;
-      const double tc[2] = {(1.0 + sig[g0 & 1] * inv_m) * inv_m, (1.0 + sig[(g0 + 1) & 1] * inv_m) * inv_m};
+#pragma unroll
+      for (int d = 0; d < kRC; ++d) {
+        const int g = g0 + min(d, D - 1);
+        rs[d] = rbuf(g);
+        cs[d] = cbuf(g);
+        tc[d] = (1.0 + sig[g % kRC] * inv_m) * inv_m;
+      }
       for_tiles(p, ntiles, pass++, &s_tile,
                 [&](int t) { replay_tile(p, t, D, write, mu_fused, rs, cs, tc, dmax, sm, ring, mu_loc); });
       stored = write;
@@ -897,14 +911,14 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[1] += t - tq; tq = t; }
 #endif
-    if (replay) reduce_phase(p, sm, rbuf[k & 1], cbuf[k & 1]);
+    if (replay) reduce_phase(p, sm, rbuf(k), cbuf(k));
     else reduce_phase(p, sm);
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[2] += t - tq; tq = t; }
 #endif
     grid.sync();
     sigma = grid_sigma(p, sm);
-    sig[k & 1] = sigma;
+    sig[k % kRC] = sigma;
     delta = grid_max(p.dlt_part, sm, 0.0f);
 #ifdef FPFP_PROJ_PROF
     { const unsigned long long t = gt(); pt[3] += t - tq; tq = t; }
@@ -913,15 +927,23 @@ __global__ void __launch_bounds__(kProjThreads, 2) proj_kernel(ProjArgs p) {
     if ((double)delta < p.eps2 || sweeps >= p.max_iter2) break;  // uniform across blocks
   }
 #if FPFP_PROJ_BULK
-  if (!stored) {   // stopped on delta after a sweep that was not stored: store Z_k (k even)
+  if (!stored) {   // stopped on delta after a sweep that was not stored: store Z_k
     const int k = sweeps;
-    const double* const rs[2] = {rbuf[(k - 1) & 1], rbuf[k & 1]};
-    const double* const cs[2] = {cbuf[(k - 1) & 1], cbuf[k & 1]};
+    const int D = (k - 2) % kRC + 1, g0 = k - D;
+    const double* rs[kRC];
+    const double* cs[kRC];
+    double tc[kRC];
     const double inv_m = 1.0 / (double)p.m;
-    const double tc[2] = {(1.0 + sig[(k - 1) & 1] * inv_m) * inv_m, 0.0};
+#pragma unroll
+    for (int d = 0; d < kRC; ++d) {
+      const int g = g0 + min(d, D - 1);
+      rs[d] = rbuf(g);
+      cs[d] = cbuf(g);
+      tc[d] = (1.0 + sig[g % kRC] * inv_m) * inv_m;
+    }
     float dd = 0.0f;
     for_tiles(p, ntiles, pass++, &s_tile,
-              [&](int t) { replay_tile(p, t, 1, true, false, rs, cs, tc, dd, sm, ring, mu_loc); });
+              [&](int t) { replay_tile(p, t, D, true, false, rs, cs, tc, dd, sm, ring, mu_loc); });
     grid.sync();
   }
 #endif
