@@ -324,7 +324,8 @@ def run_ours(args):
         "bound": "hbm", "achieved": round(proj_gbs, 1), "peak": mp["hbm_gbs"], "unit": "GB/s",
         "frac": round(proj_gbs / mp["hbm_gbs"], 4), "bytes_per_launch": pbytes,
         "bytes_rule": "SURVEY 8(d): 8 m^2 k (sweeps) + 12 n n' (finalize); sums pass, second finalize "
-                      "pass and X digit planes are overhead (in traffic)",
+                      "pass and X digit planes are overhead (in traffic); single GPU: checkpointed sweeps "
+                      "store Y after every other sweep only (DESIGN.md 6), so traffic is below these bytes",
         "ms_per_launch": round(proj_ms, 4), "share_of_step": round(proj_ms / step_ms, 4),
         "traffic": ncu_traffic("proj_kernel") if args.workload == "c5" and not sharded else None,
         "peak_source": f"{src} hbm_gbs (burst copy; the projection runs inside a long step)"}
