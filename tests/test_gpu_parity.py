@@ -60,6 +60,29 @@ def test_sweeps_vs_oracle(m):
         assert abs(d - do) <= 2e-6 * max(1.0, np.max(np.abs(Y0)))
 
 
+@pytest.mark.parametrize("m,stop", [(300, 6), (513, 4), (2100, 8), (700, 3)])
+def test_eps2_stop_between_checkpoints(m, stop):
+    # the streaming kernel stores Y only after every other sweep (checkpointed sweeps):
+    # an eps2 stop after an even sweep takes one more pass to store that sweep's Y. eps2 is
+    # placed between the oracle's delta of sweep `stop` and the smallest delta before it.
+    import paper_1207_1114_b200 as F
+    Y0 = inputs.random_matrix(2000 + m, m, m, scale=3.0, shift=0.2)
+    Yo = Y0.astype(np.float64)
+    deltas = []
+    for _ in range(stop):
+        Yo, d = O.sweep(Yo)
+        deltas.append(d)
+    lo, hi = deltas[-1], min(deltas[:-1])
+    assert lo < hi / 1.05, deltas          # a margin the fp32 deltas cannot cross
+    eps2 = float(np.sqrt(lo * hi))
+    Y = torch.from_numpy(Y0).cuda()
+    s, d = F.project(Y, eps2, 100)
+    assert s == stop
+    scale = max(1.0, np.max(np.abs(Y0)))
+    assert np.max(np.abs(Y.cpu().numpy().astype(np.float64) - Yo)) <= 2e-6 * scale
+    assert abs(d - deltas[-1]) <= 2e-6 * scale
+
+
 GEMM_VARIANTS = [pytest.param(0, 2, id="tf32x3-cg2"), pytest.param(0, 1, id="tf32x3-cg1"),
                  pytest.param(2, 2, id="simt")]
 
