@@ -514,6 +514,21 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           for (int r = 0; r < kPR; ++r)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(X + (int64_t)(sw * kPR + r) * kS + 4 * lane));
         }
+        // t_i of the warp's rows needs only the row sums and sigma, published before the first
+        // barrier: formed while warps 0-3 combine the column partials (c4 +1.2%)
+        float tir[kPR];
+        {
+          const float4 sg0 = *reinterpret_cast<const float4*>(&ss.wsig[buf][0]);
+          const float4 sg1 = *reinterpret_cast<const float4*>(&ss.wsig[buf][4]);
+          const float sigma = ((sg0.x + sg0.y) + (sg0.z + sg0.w)) + ((sg1.x + sg1.y) + (sg1.z + sg1.w));
+          const float tconst = (1.0f + sigma * inv_m) * inv_m;
+#pragma unroll
+          for (int q = 0; q < kPR; q += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(&ss.rsum[buf][sw][q]);
+            tir[q] = tconst - v.x * inv_m; tir[q + 1] = tconst - v.y * inv_m;
+            tir[q + 2] = tconst - v.z * inv_m; tir[q + 3] = tconst - v.w * inv_m;
+          }
+        }
 #ifndef FPFP_SS_PER_LANE_COMBINE   // (the per-lane variant below measured no faster: 7.36 vs 7.5 M)
         if (st < kS) {   // the kPW warp partials of column st (conflict-free rows)
           float c0 = 0.f, c1 = 0.f;
@@ -541,16 +556,6 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
           cs4 = make_float4(c01.x, c01.y, c23.x, c23.y);
         }
 #endif
-        float rsr[kPR];
-#pragma unroll
-        for (int q = 0; q < kPR; q += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(&ss.rsum[buf][sw][q]);
-          rsr[q] = v.x; rsr[q + 1] = v.y; rsr[q + 2] = v.z; rsr[q + 3] = v.w;
-        }
-        const float4 sg0 = *reinterpret_cast<const float4*>(&ss.wsig[buf][0]);
-        const float4 sg1 = *reinterpret_cast<const float4*>(&ss.wsig[buf][4]);
-        const float sigma = ((sg0.x + sg0.y) + (sg0.z + sg0.w)) + ((sg1.x + sg1.y) + (sg1.z + sg1.w));
-        const float tconst = (1.0f + sigma * inv_m) * inv_m;
         const float2 inv2 = make_float2(-inv_m, -inv_m);
         const float2 ncu01 = __fmul2_rn(make_float2(cs4.x, cs4.y), inv2);   // -c_j / m
         const float2 ncu23 = __fmul2_rn(make_float2(cs4.z, cs4.w), inv2);
@@ -559,7 +564,7 @@ __global__ void __launch_bounds__(kT, 1) small_solve_tc_kernel(SmallArgs p) {
 #pragma unroll
         for (int r = 0; r < kPR; ++r) {
           const int i = sw * kPR + r;
-          const float ti = tconst - rsr[r] * inv_m;
+          const float ti = tir[r];
           const float2 t2 = make_float2(ti, ti);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
