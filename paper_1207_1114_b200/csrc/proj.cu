@@ -53,6 +53,9 @@ struct __align__(16) ProjSmem {
 #endif
 constexpr int kSlots = FPFP_PROJ_SLOTS;   // a power of two (slot = seq % kSlots)
 static_assert((kSlots & (kSlots - 1)) == 0, "kSlots must be a power of two");
+#ifndef FPFP_PROJ_RING_FIRST
+#define FPFP_PROJ_RING_FIRST 1
+#endif
 constexpr size_t kRingBytes = FPFP_PROJ_BULK ? (size_t)kWarps * kSlots * kProjTC * sizeof(float) : 0;
 
 struct Ring {
@@ -111,6 +114,26 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   const int row1 = min(p.rows, row0 + p.TR);
   const int colbase = cb * kProjTC;
   const double inv_m = 1.0 / (double)p.m;
+#if FPFP_PROJ_BULK && FPFP_PROJ_RING_FIRST
+  // the first rows' bulk copies go out before the sum vectors are loaded (HBM and L2 latency overlap)
+  constexpr int kDepth = kSlots;
+  const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
+  float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
+  uint64_t* wbar = ring_st.bar + warp * kSlots;
+  const uint32_t seq0 = ring_st.seq;
+  const int i0 = row0 + warp;
+  const int nrows_w = i0 < row1 ? (row1 - i0 + kWarps - 1) / kWarps : 0;
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // Y written by the generic proxy
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < kDepth && k < nrows_w; ++k) {
+      const uint32_t slot = (seq0 + k) % kSlots;
+      ring_issue(wbar + slot, wbuf + slot * kProjTC, p.Y + (int64_t)(i0 + k * kWarps) * p.ldY + colbase,
+                 row_bytes);
+    }
+  }
+  __syncwarp();
+#endif
 
   double u[kQ][4], colacc[kQ][4];
   float colf[kQ][4];
@@ -141,6 +164,7 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
   // warp (memory-level parallelism is what bounds this kernel), each slot refilled with the row
   // kDepth steps ahead as soon as its own row has been corrected and stored.
 #if FPFP_PROJ_BULK
+#if !FPFP_PROJ_RING_FIRST
   constexpr int kDepth = kSlots;
   const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
   float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
@@ -158,6 +182,7 @@ __device__ __forceinline__ void tile_pass(const ProjArgs& p, int tile, double si
     }
   }
   __syncwarp();
+#endif
   // rows are processed in groups of 4 so that their 4 row sums share one transposed warp
   // reduction (6 double shuffles per 4 rows instead of 5 per row)
   for (int tg = 0; tg < nrows_w; tg += 4) {
@@ -336,6 +361,24 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
   const int row1 = min(p.rows, row0 + p.TR);
   const int colbase = cb * kProjTC;
   const double inv_m = 1.0 / (double)p.m;
+#if FPFP_PROJ_RING_FIRST
+  const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
+  float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
+  uint64_t* wbar = ring_st.bar + warp * kSlots;
+  const uint32_t seq0 = ring_st.seq;
+  const int i0 = row0 + warp;
+  const int nrows_w = i0 < row1 ? (row1 - i0 + kWarps - 1) / kWarps : 0;
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (lane == 0) {
+#pragma unroll 1
+    for (int k = 0; k < kSlots && k < nrows_w; ++k) {
+      const uint32_t slot = (seq0 + k) % kSlots;
+      ring_issue(wbar + slot, wbuf + slot * kProjTC, p.Y + (int64_t)(i0 + k * kWarps) * p.ldY + colbase,
+                 row_bytes);
+    }
+  }
+  __syncwarp();
+#endif
 
   float u[kRC][kQ][4], colf[kQ][4];
   bool inrow[kQ];
@@ -362,6 +405,7 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
     }
   }
 
+#if !FPFP_PROJ_RING_FIRST
   const uint32_t row_bytes = (uint32_t)min(kProjTC, (int)(p.ldY - colbase)) * 4u;
   float* wbuf = ring_st.buf + (size_t)warp * kSlots * kProjTC;
   uint64_t* wbar = ring_st.bar + warp * kSlots;
@@ -378,6 +422,7 @@ __device__ __forceinline__ void replay_pass(const ProjArgs& p, int tile, int D, 
     }
   }
   __syncwarp();
+#endif
   for (int tg = 0; tg < nrows_w; tg += 4) {
     double rq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
