@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 
 #include "common.cuh"
@@ -67,6 +68,58 @@ __device__ __forceinline__ bool has_tag(const ulonglong2& v, unsigned tag) {
 __device__ __forceinline__ double tagged_value(const ulonglong2& v) {
   return __longlong_as_double((long long)((v.x & 0xffffffffull) | (v.y << 32)));
 }
+
+// 8-byte records {fp32 value | tag << 32} (one single-copy-atomic word) for the partial sums of the
+// fp32 sweeps (FPFP_OC_REC32): half the bytes every CTA polls per sweep
+__device__ __forceinline__ void st_tagged32(void* dst, float v, unsigned tag) {
+  const unsigned long long w = (unsigned long long)__float_as_uint(v) | ((unsigned long long)tag << 32);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+}
+struct Rec16 {   // the fp64 record
+  using T = ulonglong2;
+  static __device__ __forceinline__ T ld(const T* p) { return ld_tagged(p); }
+  static __device__ __forceinline__ bool ok(const T& v, unsigned tag) { return has_tag(v, tag); }
+  static __device__ __forceinline__ double val(const T& v) { return tagged_value(v); }
+  static __device__ __forceinline__ T zero(unsigned tag) {
+    const unsigned long long z = (unsigned long long)tag << 32;
+    return make_ulonglong2(z, z);
+  }
+};
+struct Rec8 {    // the fp32 record
+  using T = unsigned long long;
+  static __device__ __forceinline__ T ld(const T* p) {
+    T v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ bool ok(const T& v, unsigned tag) { return (unsigned)(v >> 32) == tag; }
+  static __device__ __forceinline__ double val(const T& v) { return (double)__uint_as_float((unsigned)v); }
+  static __device__ __forceinline__ T zero(unsigned tag) { return (unsigned long long)tag << 32; }
+};
+template <class R, int N>
+__device__ __forceinline__ void issue_rec(typename R::T (&v)[N], const typename R::T* src, int64_t stride, int count,
+                                          unsigned tag) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = q < count ? R::ld(src + q * stride) : R::zero(tag);
+}
+template <class R, int N>
+__device__ __forceinline__ bool repoll_rec(typename R::T (&v)[N], const typename R::T* src, int64_t stride, unsigned tag) {
+  bool ready = true;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (!R::ok(v[q], tag)) { ready = false; v[q] = R::ld(src + q * stride); }
+  return ready;
+}
+template <class R, int N>
+__device__ __forceinline__ double sum_rec(const typename R::T (&v)[N]) {   // in q order
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < N; ++q) s += R::val(v[q]);
+  return s;
+}
+#ifndef FPFP_OC_REC32
+#define FPFP_OC_REC32 1
+#endif
 
 #ifndef FPFP_OC_POLL_NS
 #define FPFP_OC_POLL_NS 0
@@ -148,6 +201,12 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #endif
   ulonglong2* const rowq = reinterpret_cast<ulonglong2*>(p.rowp);   // [2][PC][m] records
   ulonglong2* const colq = reinterpret_cast<ulonglong2*>(p.colp);   // [2][PR][m]
+  // the fp32 sweeps' 8-byte records [2][PC][m] / [2][PR][m] live in the first half of the fp64
+  // records' storage, inside buffer 0, which only exchange 0 (the sums pass) uses as fp64: exchange
+  // x >= 2 can be written only after every CTA has absorbed exchange x - 1 >= 1, so after exchange 0;
+  // stale words there carry other tags
+  unsigned long long* const rowq8 = reinterpret_cast<unsigned long long*>(p.rowp);
+  unsigned long long* const colq8 = reinterpret_cast<unsigned long long*>(p.colp);
   ulonglong2* const totq = reinterpret_cast<ulonglong2*>(p.tot);    // [2][nb]
   ulonglong2* const dltq = reinterpret_cast<ulonglong2*>(p.dlt);    // [2][nb]
   const unsigned tag0 = p.epoch << 16;                               // tag = tag0 ^ exchange index
@@ -289,6 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         rs = (s0 + s1) + (s2 + s3);
       }
       if (nb == 1) sh.r[t] = rs;   // one tile: the sums stay on chip (the element loop is done)
+      else if (FPFP_OC_REC32 && mode == kSweep32)
+        st_tagged32(rowq8 + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, (float)rs, tag);
       else st_tagged(rowq + ((int64_t)buf * p.PC + pc) * p.m + r0 + t, rs, tag);
     }
     for (int j = threadIdx.x; j < nc; j += kThreads) {
@@ -301,6 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         for (int w = 0; w < kWarps; ++w) s += sh.colsum.d[w][j];
       }
       if (nb == 1) { sh.c[j] = s; sh.uf[j] = (float)(s * inv_m); }
+      else if (FPFP_OC_REC32 && mode == kSweep32)
+        st_tagged32(colq8 + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, (float)s, tag);
       else st_tagged(colq + ((int64_t)buf * p.PR + pr) * p.m + c0 + j, s, tag);
     }
 #ifdef FPFP_OC_PROF
@@ -317,35 +380,41 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   constexpr int kMaxTilesPerLane = 5;   // PR * PC <= 160
   constexpr int kMaxP = 12;             // PR, PC <= 12
   constexpr bool kSplit = kThreads >= 512;
-  auto absorb = [&](int buf, unsigned tag, double& sigma, float& delta) {
+  // R: the record type of the row / column partials (Rec16, or Rec8 for the fp32 sweeps)
+  auto absorb = [&](auto rec, int buf, unsigned tag, double& sigma, float& delta) {
+    using R = decltype(rec);
+    using RT = typename R::T;
     const int t = threadIdx.x;
-    const ulonglong2* rsrc = rowq + (int64_t)buf * p.PC * p.m + r0 + t;
-    const ulonglong2* csrc = colq + (int64_t)buf * p.PR * p.m + c0 + (kSplit ? t - kThreads / 2 : t);
+    const RT* rbase = std::is_same<R, Rec8>::value ? reinterpret_cast<const RT*>(rowq8) : reinterpret_cast<const RT*>(rowq);
+    const RT* cbase = std::is_same<R, Rec8>::value ? reinterpret_cast<const RT*>(colq8) : reinterpret_cast<const RT*>(colq);
+    const RT* rsrc = rbase + (int64_t)buf * p.PC * p.m + r0 + t;
+    const RT* csrc = cbase + (int64_t)buf * p.PR * p.m + c0 + (kSplit ? t - kThreads / 2 : t);
     const ulonglong2* tsrc = totq + buf * nb + lane;
     const ulonglong2* dsrc = dltq + buf * nb + lane;
     const int tw = kSplit ? kWarps / 2 - 1 : kWarps - 1;   // the warp that sums the tile totals
     if (kSplit && t >= kThreads / 2) {
-      ulonglong2 cv[kMaxP];
+      RT cv[kMaxP];
       const int nq = t - kThreads / 2 < nc ? p.PR : 0;
-      issue_tagged(cv, csrc, p.m, nq, tag);
-      while (!repoll_tagged(cv, csrc, p.m, tag)) poll_backoff();
+      issue_rec<R>(cv, csrc, p.m, nq, tag);
+      while (!repoll_rec<R>(cv, csrc, p.m, tag)) poll_backoff();
       __syncwarp();
       if (nq) {
-        const double cs = sum_tagged(cv);
+        const double cs = sum_rec<R>(cv);
         sh.c[t - kThreads / 2] = cs;
         sh.uf[t - kThreads / 2] = (float)(cs * inv_m);
       }
     } else {
-      ulonglong2 rv[kMaxP], cv[kSplit ? 1 : kMaxP], tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
+      RT rv[kMaxP], cv[kSplit ? 1 : kMaxP];
+      ulonglong2 tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
       const int nr_q = t < nr ? p.PC : 0, nc_q = (!kSplit && t < nc) ? p.PR : 0;
       const int nt_q = warp == tw ? (nb - lane + 31) / 32 : 0;   // tiles lane, lane + 32, ...
-      issue_tagged(rv, rsrc, p.m, nr_q, tag);
-      issue_tagged(cv, csrc, p.m, nc_q, tag);
+      issue_rec<R>(rv, rsrc, p.m, nr_q, tag);
+      issue_rec<R>(cv, csrc, p.m, nc_q, tag);
       issue_tagged(tv, tsrc, 32, nt_q, tag);
       issue_tagged(dv, dsrc, 32, nt_q, tag);
       for (;;) {
-        bool ready = repoll_tagged(rv, rsrc, p.m, tag);
-        ready &= repoll_tagged(cv, csrc, p.m, tag);
+        bool ready = repoll_rec<R>(rv, rsrc, p.m, tag);
+        ready &= repoll_rec<R>(cv, csrc, p.m, tag);
         ready &= repoll_tagged(tv, tsrc, 32, tag);
         ready &= repoll_tagged(dv, dsrc, 32, tag);
         if (ready) break;
@@ -356,9 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       // next element loop can run with its warps split (measured at c2: 5.2 us per sweep with
       // neither, 4.6 with this one only, 3.5 with both)
       __syncwarp();
-      if (nr_q) sh.r[t] = sum_tagged(rv);
+      if (nr_q) sh.r[t] = sum_rec<R>(rv);
       if (nc_q) {
-        const double cs = sum_tagged(cv);
+        const double cs = sum_rec<R>(cv);
         sh.c[t] = cs;
         sh.uf[t] = (float)(cs * inv_m);
       }
@@ -378,19 +447,20 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   };
 
   // a single tile (m <= FPFP_OC_SINGLE_TILE) needs no exchange: its sums are already in shared memory
-  auto exchange = [&](int bufx, unsigned tag, double& sigma_, float& delta_) {
+  auto exchange = [&](int bufx, unsigned tag, double& sigma_, float& delta_, bool rec32) {
     if (nb == 1) {
       __syncthreads();
       sigma_ = sh.bc[0];
       delta_ = (float)sh.bc[1];
       return;
     }
-    absorb(bufx, tag, sigma_, delta_);
+    if (FPFP_OC_REC32 && rec32) absorb(Rec8{}, bufx, tag, sigma_, delta_);
+    else absorb(Rec16{}, bufx, tag, sigma_, delta_);
   };
   double sigma;
   float delta;
   pass(kSums, 0, tag0, 0.0);               // exchange 0: the sums of the incoming Y
-  exchange(0, tag0, sigma, delta);
+  exchange(0, tag0, sigma, delta, false);
 
   int sweeps = 0;
 #ifdef FPFP_OC_PROF
@@ -403,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
 #ifdef FPFP_OC_PROF
     const long long b0_ = clock64();
 #endif
-    exchange((int)(x & 1), tag0 ^ (x & 0xffffu), sigma, delta);
+    exchange((int)(x & 1), tag0 ^ (x & 0xffffu), sigma, delta, sweeps > 0);
 #ifdef FPFP_OC_PROF
     pc_abs += clock64() - b0_;
 #endif
