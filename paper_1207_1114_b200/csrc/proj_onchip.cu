@@ -120,6 +120,9 @@ __device__ __forceinline__ double sum_rec(const typename R::T (&v)[N]) {   // in
 #ifndef FPFP_OC_REC32
 #define FPFP_OC_REC32 1
 #endif
+#ifndef FPFP_OC_TOT32   // the fp32 sweeps' tile totals and deltas as 8-byte records too
+#define FPFP_OC_TOT32 0
+#endif
 
 #ifndef FPFP_OC_POLL_NS
 #define FPFP_OC_POLL_NS 0
@@ -207,6 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
   // stale words there carry other tags
   unsigned long long* const rowq8 = reinterpret_cast<unsigned long long*>(p.rowp);
   unsigned long long* const colq8 = reinterpret_cast<unsigned long long*>(p.colp);
+  unsigned long long* const totq8 = reinterpret_cast<unsigned long long*>(p.tot);   // (FPFP_OC_TOT32)
+  unsigned long long* const dltq8 = reinterpret_cast<unsigned long long*>(p.dlt);
   ulonglong2* const totq = reinterpret_cast<ulonglong2*>(p.tot);    // [2][nb]
   ulonglong2* const dltq = reinterpret_cast<ulonglong2*>(p.dlt);    // [2][nb]
   const unsigned tag0 = p.epoch << 16;                               // tag = tag0 ^ exchange index
@@ -319,8 +324,13 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         sh.bc[0] = t;
         sh.bc[1] = (double)d;
       } else {
-        st_tagged(totq + buf * nb + b, t, tag);
-        st_tagged(dltq + buf * nb + b, (double)d, tag);
+        if (FPFP_OC_TOT32 && mode == kSweep32) {
+          st_tagged32(totq8 + buf * nb + b, (float)t, tag);
+          st_tagged32(dltq8 + buf * nb + b, d, tag);
+        } else {
+          st_tagged(totq + buf * nb + b, t, tag);
+          st_tagged(dltq + buf * nb + b, (double)d, tag);
+        }
       }
     }
 #ifdef FPFP_OC_PROF
@@ -389,8 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
     const RT* cbase = std::is_same<R, Rec8>::value ? reinterpret_cast<const RT*>(colq8) : reinterpret_cast<const RT*>(colq);
     const RT* rsrc = rbase + (int64_t)buf * p.PC * p.m + r0 + t;
     const RT* csrc = cbase + (int64_t)buf * p.PR * p.m + c0 + (kSplit ? t - kThreads / 2 : t);
-    const ulonglong2* tsrc = totq + buf * nb + lane;
-    const ulonglong2* dsrc = dltq + buf * nb + lane;
+    using TR = typename std::conditional<FPFP_OC_TOT32 && std::is_same<R, Rec8>::value, Rec8, Rec16>::type;
+    using TT = typename TR::T;
+    const TT* tsrc = (std::is_same<TR, Rec8>::value ? reinterpret_cast<const TT*>(totq8)
+                                                     : reinterpret_cast<const TT*>(totq)) + buf * nb + lane;
+    const TT* dsrc = (std::is_same<TR, Rec8>::value ? reinterpret_cast<const TT*>(dltq8)
+                                                     : reinterpret_cast<const TT*>(dltq)) + buf * nb + lane;
     const int tw = kSplit ? kWarps / 2 - 1 : kWarps - 1;   // the warp that sums the tile totals
     if (kSplit && t >= kThreads / 2) {
       RT cv[kMaxP];
@@ -405,18 +419,18 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
       }
     } else {
       RT rv[kMaxP], cv[kSplit ? 1 : kMaxP];
-      ulonglong2 tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
+      TT tv[kMaxTilesPerLane], dv[kMaxTilesPerLane];
       const int nr_q = t < nr ? p.PC : 0, nc_q = (!kSplit && t < nc) ? p.PR : 0;
       const int nt_q = warp == tw ? (nb - lane + 31) / 32 : 0;   // tiles lane, lane + 32, ...
       issue_rec<R>(rv, rsrc, p.m, nr_q, tag);
       issue_rec<R>(cv, csrc, p.m, nc_q, tag);
-      issue_tagged(tv, tsrc, 32, nt_q, tag);
-      issue_tagged(dv, dsrc, 32, nt_q, tag);
+      issue_rec<TR>(tv, tsrc, 32, nt_q, tag);
+      issue_rec<TR>(dv, dsrc, 32, nt_q, tag);
       for (;;) {
         bool ready = repoll_rec<R>(rv, rsrc, p.m, tag);
         ready &= repoll_rec<R>(cv, csrc, p.m, tag);
-        ready &= repoll_tagged(tv, tsrc, 32, tag);
-        ready &= repoll_tagged(dv, dsrc, 32, tag);
+        ready &= repoll_rec<TR>(tv, tsrc, 32, tag);
+        ready &= repoll_rec<TR>(dv, dsrc, 32, tag);
         if (ready) break;
         poll_backoff();
       }
@@ -432,10 +446,10 @@ __global__ void __launch_bounds__(kThreads, 1) proj_onchip_kernel(OnchipArgs p) 
         sh.uf[t] = (float)(cs * inv_m);
       }
       if (warp == tw) {   // (converged: __syncwarp above)
-        double sv = sum_tagged(tv);
+        double sv = sum_rec<TR>(tv);
         float d = 0.0f;
 #pragma unroll
-        for (int u = 0; u < kMaxTilesPerLane; ++u) d = fmaxf(d, (float)tagged_value(dv[u]));
+        for (int u = 0; u < kMaxTilesPerLane; ++u) d = fmaxf(d, (float)TR::val(dv[u]));
         sv = warp_sum(sv);
         d = warp_max(d);
         if (lane == 0) { sh.bc[0] = sv; sh.bc[1] = (double)d; }
