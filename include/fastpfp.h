@@ -311,8 +311,9 @@ const char* fastpfp_batched_last_error(const fastpfp_batched* h);
 
 /* One projection sweep (Algorithm 1 lines 5-6) applied k times in place to the m x m
  * matrix Y (device, dense, ld = m), stopping early when max|dY| < eps2. *sweeps_out,
- * *delta_out (host) receive the count and the last delta. Row/column sums and the P1 correction
- * are evaluated in fp64. */
+ * *delta_out (host) receive the count and the last delta. Row/column sums are combined in fp64;
+ * the first sweep's P1 correction is fp64, the later sweeps' fp32 (checkpointed sweeps: Y stored
+ * every other sweep). */
 int fastpfp_project(float* Y, int64_t m, double eps2, int32_t max_iter2, int32_t* sweeps_out,
                     double* delta_out, int64_t stream);
 
