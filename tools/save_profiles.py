@@ -68,6 +68,9 @@ for key, suffix, desc in caps:
     rep = os.path.join(G, f"{tag}_{suffix}.ncu-rep")
     if os.path.exists(rep):
         args += [key, rep, desc]
+        # the full raw page travels with profiles/ (the .ncu-rep itself stays in the scratch gpurun_out/)
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        open(os.path.join(P, f"{rnd}_ncu_raw_{suffix}.csv"), "w").write(raw)
 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summarize.py"), *args], check=True,
                stdout=subprocess.DEVNULL)
 print("saved", tag, "->", rnd)
